@@ -1,0 +1,429 @@
+#!/usr/bin/env python
+"""Benchmark of the B200-native Harpia hot path (BASELINE.json configs[1]).
+
+Workload (one "step"): the 3x3x3 median (r=1) AND the 3x3x3 mean (r=1) over a
+1024^3 float32 synthetic volume per GPU — BASELINE.json configs[1]
+("3x3x3 median and 3D mean filter on a 1024^3 float32 volume, chunked with
+halos").  ``value`` = output voxels of both filters per second, whole job
+(all ranks), device-resident inputs; ``e2e`` = the same step through the
+public API ``registry.run_operator`` from pinned host memory with a budget
+that forces >= 4 halo'd chunks (host->device and device->host inside the
+timed region).  Multi-GPU: weak scaling, one 1024-slice z-slab per rank, no
+data-path collective (each rank owns its padded range).
+
+``--impl reference`` times the reference algorithm on the host cores instead
+(the CPU restatement in oracle/, all threads; the reference itself is Python
+over scipy and does not travel to the GPU box) on a bounded slab sample.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "Gvoxel/s per filter (3D Gaussian, median) at 1/2/4/8 B200; % HBM roofline"
+UNIT = "Gvoxel/s"
+BYTES_PER_VOXEL = 8  # f32 in + f32 out
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--size", type=int, default=1024, help="edge of the per-GPU cube")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--extra", action="store_true", help="also time gaussian/erode breakdown")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        p = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def traffic_from_profiles():
+    """dram bytes per launch of the dominant kernel from the committed ncu capture."""
+    try:
+        t = json.loads((ROOT / "profiles" / "traffic.json").read_text())
+        return t
+    except Exception:
+        return {}
+
+
+# --------------------------------------------------------------------------
+# clocks sampler (B200_PROFILING.md "clocks DURING the timed region")
+# --------------------------------------------------------------------------
+class Clocks:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap,utilization.gpu")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+        return False
+
+    def summary(self):
+        rows = []
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                rows.append((float(parts[0]), float(parts[1]), parts[2:6], float(parts[6])))
+            except ValueError:
+                continue
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        loaded = [r for r in rows if r[3] > 0] or rows
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in loaded for i, v in enumerate(r[2]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(r[0] for r in loaded),
+                "sm_max_mhz": max(r[1] for r in rows), "reasons": reasons,
+                "samples": len(loaded)}
+
+
+# --------------------------------------------------------------------------
+# distributed plumbing
+# --------------------------------------------------------------------------
+def dist_setup(args):
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(local)
+    os.environ["HARPIA_DEVICE"] = str(local)
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def max_over_ranks(world, value: float) -> float:
+    if world == 1:
+        return value
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([value], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# --------------------------------------------------------------------------
+# CPU reference arm / baseline (the oracle restatement, all host threads)
+# --------------------------------------------------------------------------
+def cpu_sample_run(slices: int, yx: int, seed: int = 0):
+    from oracle import oracle as O
+
+    rng = np.random.default_rng(seed)
+    x = rng.random((slices + 2, yx, yx), dtype=np.float32)  # +1 halo slice each side
+    t0 = time.perf_counter()
+    O.median(x, 1)
+    t1 = time.perf_counter()
+    O.mean(x, 1)
+    t2 = time.perf_counter()
+    return (t1 - t0), (t2 - t1), slices * yx * yx
+
+
+def calibrate_cpu(yx: int, target_s: float = 4.0) -> int:
+    tm, tmean, vox = cpu_sample_run(1, yx)
+    per_slice = (tm + tmean) / 1  # seconds per output slice (both filters), upper bound
+    return int(max(1, min(64, target_s / max(per_slice, 1e-6))))
+
+
+def cpu_baseline(args, yx):
+    from oracle import oracle as O
+
+    slices = calibrate_cpu(yx, target_s=5.0)
+    runs = [cpu_sample_run(slices, yx, seed=s) for s in range(2)]
+    best = min(r[0] + r[1] for r in runs)
+    vox = runs[0][2]
+    return {"value": round(2 * vox / best / 1e9, 6), "unit": UNIT, "cores": O.num_threads(),
+            "kind": "port",
+            "sample": f"median r=1 + mean r=1 on a {slices}x{yx}x{yx} f32 slab (+1 halo slice "
+                      f"each side) of the same U[0,1) workload, oracle/harpia_oracle.c with "
+                      f"{O.num_threads()} OpenMP threads, best of 2",
+            "median_mvox_s": round(vox / min(r[0] for r in runs) / 1e6, 3),
+            "mean_mvox_s": round(vox / min(r[1] for r in runs) / 1e6, 3)}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from oracle import oracle as O
+
+    yx = args.size
+    slices = calibrate_cpu(yx, target_s=3.0)
+    for _ in range(args.warmup):
+        cpu_sample_run(slices, yx)
+    times = []
+    vox = 0
+    for k in range(args.steps):
+        tm, tmean, vox = cpu_sample_run(slices, yx, seed=k)
+        times.append(tm + tmean)
+    total = sum(times)
+    value = 2 * vox * args.steps / total / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * total / args.steps, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"median r=1 + mean r=1, {yx}^3 f32 (BASELINE configs[1]), "
+                               f"bounded CPU sample of {slices} slices per step",
+                   "global_batch": 1, "seq_len": yx},
+        "cpu_baseline": {"value": round(value, 6), "unit": UNIT, "cores": O.num_threads(),
+                         "kind": "port",
+                         "sample": f"{slices}x{yx}x{yx} f32 slab per step (+1 halo slice each side)"},
+        "e2e": {"value": round(value, 6), "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------------
+# GPU arm
+# --------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+
+    from paper_2511_11890_b200 import _native, filters, registry
+    from paper_2511_11890_b200.chunking import MemoryBudget
+
+    world, rank, local = dist_setup(args)
+    n = args.size
+    shape = (n, n, n)
+    vox = n * n * n
+    gen = torch.Generator(device="cuda").manual_seed(1000 + rank)
+    # padded block: 1 halo slice each side (radius 1); inputs >> L2 (4 GiB vs 126 MB)
+    x = torch.rand((n + 2, n, n), generator=gen, device="cuda", dtype=torch.float32)
+    out_med = torch.empty(shape, device="cuda", dtype=torch.float32)
+    out_mean = torch.empty(shape, device="cuda", dtype=torch.float32)
+    p_med = filters.median_program(1)
+    p_mean = filters.mean_program(1)
+    stream = torch.cuda.current_stream()
+
+    launches = [0]
+
+    def step():
+        launches[0] += _native.apply_device(x, out_med, p_med, 1, stream)
+        launches[0] += _native.apply_device(x, out_mean, p_mean, 1, stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    barrier(world)
+    torch.cuda.synchronize()
+    launches[0] = 0
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        start.record(stream)
+        for k in range(args.steps):
+            ev[k][0].record(stream)
+            launches[0] += _native.apply_device(x, out_med, p_med, 1, stream)
+            ev[k][1].record(stream)
+            launches[0] += _native.apply_device(x, out_mean, p_mean, 1, stream)
+            ev[k][2].record(stream)
+        end.record(stream)
+        torch.cuda.synchronize()
+    barrier(world)
+    torch.cuda.synchronize()
+    ms_local = start.elapsed_time(end)
+    ms = max_over_ranks(world, ms_local)
+    med_ms = statistics.mean(e[0].elapsed_time(e[1]) for e in ev)
+    mean_ms = statistics.mean(e[1].elapsed_time(e[2]) for e in ev)
+    value = world * 2 * vox * args.steps / (ms * 1e-3) / 1e9
+    gpu_launches = launches[0]
+    clocks = clk.summary()
+    peak, peak_kind = peaks()
+    dominant = "median" if med_ms >= mean_ms else "mean"
+    dom_ms = max(med_ms, mean_ms)
+    achieved = BYTES_PER_VOXEL * vox / (dom_ms * 1e-3) / 1e9
+    tr = traffic_from_profiles().get(dominant)
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": tr,
+                "kernel": f"{dominant} r=1 ({'k_median_forgetful' if dominant == 'median' else 'k_axis_pass x3'})",
+                "peak_kind": peak_kind,
+                "algorithmic_bytes_per_launch": BYTES_PER_VOXEL * vox}
+    filters_out = {
+        "median_r1": {"gvox_s": round(vox / (med_ms * 1e-3) / 1e9, 3), "ms": round(med_ms, 3),
+                      "hbm_frac": round(BYTES_PER_VOXEL * vox / (med_ms * 1e-3) / 1e9 / peak, 4)},
+        "mean_r1": {"gvox_s": round(vox / (mean_ms * 1e-3) / 1e9, 3), "ms": round(mean_ms, 3),
+                    "hbm_frac": round(BYTES_PER_VOXEL * vox / (mean_ms * 1e-3) / 1e9 / peak, 4)},
+    }
+    del x, out_med, out_mean
+    torch.cuda.synchronize()
+
+    if args.extra:
+        filters_out.update(extra_breakdown(n, peak))
+
+    # ---------------- e2e through the public API (pinned host memory) -------------
+    e2e = None
+    if not args.no_e2e:
+        host_in = torch.empty(shape, dtype=torch.float32, pin_memory=True)
+        host_in.copy_(torch.rand(shape, generator=gen, device="cuda", dtype=torch.float32).cpu())
+        xin = host_in.numpy()
+        o1 = torch.empty(shape, dtype=torch.float32, pin_memory=True).numpy()
+        o2 = torch.empty(shape, dtype=torch.float32, pin_memory=True).numpy()
+        op = registry.get_operator("median")
+        prof = op.profile({"radius": 1})
+        t = n // 4 + 2 * prof.halo_z
+        budget = MemoryBudget(int(t * prof.scratch_factor * n * n * 4) + 1, 1.0)
+        reps = []
+
+        def e2e_step():
+            _, r1 = registry.run_operator(xin, "median", {"radius": 1}, budget, out=o1)
+            _, r2 = registry.run_operator(xin, "mean", {"radius": 1}, budget, out=o2)
+            return r1, r2
+
+        for _ in range(max(1, args.warmup)):
+            e2e_step()
+        barrier(world)
+        e2e_steps = max(1, min(args.steps, 5))
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            reps.append(e2e_step())
+        t_local = time.perf_counter() - t0
+        barrier(world)
+        t_e2e = max_over_ranks(world, t_local)
+        r1, r2 = reps[-1]
+        e2e = {"value": round(world * 2 * vox * e2e_steps / t_e2e / 1e9, 4), "unit": UNIT,
+               "h2d_bytes_per_step": int(r1.h2d_bytes + r2.h2d_bytes),
+               "d2h_bytes_per_step": int(r1.d2h_bytes + r2.d2h_bytes),
+               "chunks_per_op": r1.chunk_count, "steps": e2e_steps,
+               "path": "registry.run_operator -> hb_run (pinned in/out, 4+ chunks, halos)"}
+        gpu_launches += sum(a.kernel_launches + b.kernel_launches for a, b in reps)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(args, n)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (torch.rand U[0,1) f32, seed 1000+rank)",
+            "config": {"workload": f"median r=1 + mean r=1 on {n}^3 float32 per GPU "
+                                   f"(BASELINE configs[1]); value = output voxels of both filters/s",
+                       "global_batch": world, "seq_len": n,
+                       "parallelism": f"z-slab x{world} (weak, no collective)",
+                       "l2": "inputs (4 GiB) larger than L2 (126 MB); no flush needed"},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": gpu_launches, "clocks": clocks, "filters": filters_out,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+    return 0
+
+
+def extra_breakdown(n, peak):
+    """Per-filter device-resident timings beyond the headline step."""
+    import torch
+
+    from paper_2511_11890_b200 import _native, filters, morphology
+
+    res = {}
+    stream = torch.cuda.current_stream()
+
+    def timeit(fn, reps=5):
+        fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(reps):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / reps
+
+    for edge, sigma in ((256, 2.0), (n, 2.0)):
+        x = torch.rand((edge + 16, edge, edge), device="cuda")
+        o = torch.empty((edge, edge, edge), device="cuda")
+        for prec in ("fast", "exact"):
+            prog = filters.gaussian_program(sigma, prec)
+            ms = timeit(lambda: _native.apply_device(x, o, prog, 8, stream))
+            v = edge ** 3
+            res[f"gaussian_s2_{edge}_{prec}"] = {"gvox_s": round(v / ms / 1e6, 3), "ms": round(ms, 3),
+                                                 "hbm_frac": round(8 * v / ms / 1e6 / peak, 4)}
+        del x, o
+    u = torch.randint(0, 65535, (n + 6, n, n), device="cuda", dtype=torch.int32).to(torch.uint16)
+    ou = torch.empty((n, n, n), device="cuda", dtype=torch.uint16)
+    prog = morphology.morph_program("erode", morphology.StructuringElement.ball(3))
+    ms = timeit(lambda: _native.apply_device(u, ou, prog, 3, stream))
+    res[f"erode_ball3_u16_{n}"] = {"gvox_s": round(n ** 3 / ms / 1e6, 3), "ms": round(ms, 3),
+                                   "hbm_frac": round(4 * n ** 3 / ms / 1e6 / peak, 4)}
+    del u, ou
+    torch.cuda.synchronize()
+    return res
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,182 @@
+/*
+ * harpia_b200.h — C ABI of the B200-native Harpia map-operator hot path.
+ *
+ * The reference (a pure-Python package, /root/reference/pkg/src/harpia) has no
+ * FFI; its hot path is the Python call chain
+ *
+ *     registry.run_operator            (registry.py:82-103)
+ *       -> chunking.execute_chunked    (chunking.py:215-279)
+ *         -> fn(block, params, aux)    (chunking.py:257), e.g. filters.gaussian
+ *
+ * Each entry point below replaces one piece of that chain; the Python mirror in
+ * paper_2511_11890_b200/ binds them with ctypes:
+ *
+ *   hb_run            replaces execute_chunked's chunk loop + every per-chunk fn
+ *                     (chunking.py:242-274) for a chain of map operators, on
+ *                     caller-owned HOST buffers (C-contiguous Z,Y,X).
+ *   hb_apply_device   replaces one fn(block, ...) call (chunking.py:257) on a
+ *                     DEVICE-resident block (torch tensors, sharded slabs).
+ *   hb_device_info    replaces probe_free_bytes (chunking.py:57-61): free bytes
+ *                     come from cudaMemGetInfo instead of psutil.
+ *   hb_gaussian_weights restates _gaussian_kernel (filters.py:26-30).
+ *   hb_se_*           restate StructuringElement.ball/box/cross (morphology.py:49-82)
+ *                     as offset lists (used for self-checks; Python builds offsets).
+ *
+ * Status codes map 1:1 onto the reference exception hierarchy (errors.py:4-41);
+ * see hb_status.  No torch types cross this boundary: plain pointers and sizes.
+ */
+#ifndef HARPIA_B200_H
+#define HARPIA_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HB_ABI_VERSION 1
+
+/* errors.py:4-41 */
+typedef enum {
+  HB_OK = 0,
+  HB_EPARAM = 1,              /* ParameterError            errors.py:8        */
+  HB_EBUDGET_SMALL = 2,       /* BudgetTooSmallError       errors.py:24-29    */
+  HB_EBUDGET_UNAVAILABLE = 3, /* BudgetUnavailableError    errors.py:20       */
+  HB_ECHUNK = 4,              /* ChunkExecutionError       errors.py:32-37    */
+  HB_ECANCELLED = 5,          /* JobCancelled              errors.py:40-41    */
+  HB_ECUDA = 6,               /* ChunkExecutionError (device fault) / no GPU  */
+  HB_EUNSUPPORTED = 7         /* UnsupportedFormatError    errors.py:16       */
+} hb_status;
+
+/* volume.py:17-23 SUPPORTED_DTYPES + LABEL_DTYPE */
+typedef enum { HB_U8 = 0, HB_U16 = 1, HB_U32 = 2, HB_F32 = 3 } hb_dtype;
+
+typedef enum { HB_HOST = 0, HB_DEVICE = 1 } hb_location;
+
+/* A C-contiguous (Z, Y, X) volume, x fastest (volume.py:1-5). */
+typedef struct {
+  void* data;
+  int32_t dtype;     /* hb_dtype */
+  int32_t location;  /* hb_location */
+  int64_t nz, ny, nx;
+} hb_volume;
+
+/* Map operators on the hot path (registry.py:135-191, 234-246, 274-285). */
+typedef enum {
+  HB_OP_IDENTITY = 0, /* registry.py:127-133 */
+  HB_OP_GAUSSIAN = 1, /* filters.py:33-41    */
+  HB_OP_MEAN = 2,     /* filters.py:66-75    */
+  HB_OP_MEDIAN = 3,   /* filters.py:78-82    */
+  HB_OP_UNSHARP = 4,  /* filters.py:136-139  */
+  HB_OP_LOG = 5,      /* hessian trace, filters.py:234-264 */
+  HB_OP_ERODE = 6,    /* morphology.py:114-116 */
+  HB_OP_DILATE = 7    /* morphology.py:119-121 (caller passes the SE; the
+                         library reflects it, as the reference does) */
+} hb_op;
+
+typedef enum {
+  HB_PREC_FAST = 0,  /* fp32 accumulation, within 1e-5 of the reference */
+  HB_PREC_EXACT = 1  /* fp64 per pass + f32 round: bit-exact Gaussian */
+} hb_precision;
+
+/* One stage of a (possibly chained) map pipeline.  open/close/iterations are
+ * expressed as chains of erode/dilate stages (morphology.py:124-140). */
+typedef struct {
+  int32_t op;          /* hb_op */
+  int32_t precision;   /* hb_precision (gaussian/unsharp/log) */
+  double sigma;        /* gaussian/unsharp/log */
+  double amount;       /* unsharp */
+  int32_t radius;      /* mean/median */
+  int32_t n_offsets;   /* erode/dilate: number of (dz,dy,dx) triples */
+  const int32_t* offsets; /* erode/dilate: 3*n_offsets ints, must contain origin */
+  int32_t n_weights;   /* gaussian/unsharp/log: 2*ceil(4 sigma)+1, or 0 */
+  const float* weights; /* optional f32 taps from the caller's _gaussian_kernel
+                           (filters.py:26-30); NULL = computed by the library */
+} hb_stage;
+
+/* One chunk of a ChunkPlan (chunking.py:93-111): interior [z_start, z_stop),
+ * halos already truncated at the volume faces. */
+typedef struct {
+  int64_t z_start, z_stop, halo_lo, halo_hi;
+} hb_chunk;
+
+typedef int32_t (*hb_cancel_fn)(void* ctx); /* nonzero => cancel */
+
+typedef struct {
+  int32_t device;            /* CUDA ordinal */
+  int32_t pipeline_depth;    /* chunks in flight (1 = serial, 2 = double buffer; 0 = auto) */
+  int64_t device_budget;     /* cap on executor device bytes (0 = no cap) */
+  hb_cancel_fn cancel;       /* polled before every chunk (chunking.py:245-246) */
+  void* cancel_ctx;
+  double* chunk_seconds;     /* optional out array [nchunks] (chunking.py:274) */
+  int32_t fault_chunk;       /* test hook: fail chunk i with HB_ECHUNK (-1 = off) */
+  int32_t host_threads;      /* threads for pageable<->pinned staging (0 = auto) */
+} hb_exec;
+
+typedef struct {
+  int64_t chunk_count;
+  int64_t failed_chunk;        /* ChunkExecutionError.chunk_index, -1 if none */
+  int64_t minimum_bytes;       /* BudgetTooSmallError.minimum_bytes */
+  int64_t device_peak_bytes;   /* executor high-water mark of device bytes */
+  int64_t device_residual_bytes; /* executor bytes still held at return (must be 0) */
+  int64_t h2d_bytes, d2h_bytes;
+  double h2d_ms, kernel_ms, d2h_ms, wall_ms;
+  int64_t kernel_launches;
+  char message[512];
+} hb_report;
+
+/* Library / device introspection ----------------------------------------- */
+int32_t hb_abi_version(void);
+const char* hb_version(void);
+/* hb_status; free/total bytes of device `dev` (chunking.py:57-61 analogue). */
+int32_t hb_device_info(int32_t dev, int64_t* free_bytes, int64_t* total_bytes);
+int32_t hb_device_count(void);
+
+/* Parameter helpers ------------------------------------------------------- */
+/* ceil(4*sigma) (filters.py:21-23) */
+int32_t hb_gaussian_radius(double sigma);
+/* Writes 2r+1 float32 weights of _gaussian_kernel (filters.py:26-30). */
+int32_t hb_gaussian_weights(double sigma, float* out, int32_t capacity);
+/* Z dependence radius of a stage chain (sum of per-stage halos, registry.py). */
+int64_t hb_chain_halo(const hb_stage* stages, int32_t nstages);
+
+/* Execution --------------------------------------------------------------- */
+/* Chunked streaming executor over HOST volumes: for every chunk, upload the
+ * padded slab, run the stage chain on the device, download the interior.
+ * `out` must be a host volume of the chain's output dtype and in's shape. */
+int32_t hb_run(const hb_volume* in, hb_volume* out,
+               const hb_stage* stages, int32_t nstages,
+               const hb_chunk* chunks, int64_t nchunks,
+               const hb_exec* ex, hb_report* rep);
+
+/* Apply a stage chain to a DEVICE block `in` (clamp-to-edge at all its faces)
+ * and write output slices [z_begin, z_begin + out->nz) of the block into `out`
+ * (a device volume with out->ny == in->ny, out->nx == in->nx).  Runs on
+ * `stream` (cudaStream_t, NULL = legacy default); asynchronous unless
+ * `synchronize` is nonzero.  Device temporaries come from a library-private
+ * pool that is trimmed to zero before return. */
+int32_t hb_apply_device(const hb_volume* in, hb_volume* out,
+                        const hb_stage* stages, int32_t nstages,
+                        int64_t z_begin, void* stream, int32_t synchronize,
+                        hb_report* rep);
+
+/* Output dtype of a chain for a given input dtype (hb_dtype), or -1. */
+int32_t hb_chain_out_dtype(const hb_stage* stages, int32_t nstages, int32_t in_dtype);
+
+/* Trim the library's private device pool of `dev` to zero bytes (after
+ * asynchronous hb_apply_device calls; synchronous jobs trim themselves). */
+int32_t hb_trim_device(int32_t dev);
+/* Bytes currently reserved by the library's private pool on `dev`. */
+int64_t hb_device_pool_bytes(int32_t dev);
+
+/* Pinned-host helpers (cudaHostRegister for the duration of a job). */
+int32_t hb_pin(void* ptr, int64_t bytes);
+int32_t hb_unpin(void* ptr);
+
+/* Last error message of the calling thread. */
+const char* hb_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HARPIA_B200_H */

@@ -1,0 +1,370 @@
+"""ctypes binding of the C ABI in include/harpia_b200.h.
+
+This module is the only door into the device code.  There is no CPU fallback:
+if ``_lib/libharpia_b200.so`` is missing or no CUDA device is present, every
+compute entry point raises (``RuntimeError`` for a missing library,
+``BudgetUnavailableError`` for a missing device).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+from dataclasses import dataclass, field
+from pathlib import Path
+from typing import Callable, Optional, Sequence
+
+import numpy as np
+
+from .errors import HB_OK, ParameterError, UnsupportedFormatError, raise_for_status
+
+LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libharpia_b200.so"
+
+# enum values of include/harpia_b200.h
+HB_U8, HB_U16, HB_U32, HB_F32 = 0, 1, 2, 3
+HB_HOST, HB_DEVICE = 0, 1
+OP_IDENTITY, OP_GAUSSIAN, OP_MEAN, OP_MEDIAN, OP_UNSHARP, OP_LOG, OP_ERODE, OP_DILATE = range(8)
+PREC_FAST, PREC_EXACT = 0, 1
+
+DTYPE_CODE = {
+    np.dtype("uint8"): HB_U8,
+    np.dtype("uint16"): HB_U16,
+    np.dtype("uint32"): HB_U32,
+    np.dtype("float32"): HB_F32,
+}
+CODE_DTYPE = {v: k for k, v in DTYPE_CODE.items()}
+
+
+class HbVolume(ctypes.Structure):
+    _fields_ = [
+        ("data", ctypes.c_void_p),
+        ("dtype", ctypes.c_int32),
+        ("location", ctypes.c_int32),
+        ("nz", ctypes.c_int64),
+        ("ny", ctypes.c_int64),
+        ("nx", ctypes.c_int64),
+    ]
+
+
+class HbStage(ctypes.Structure):
+    _fields_ = [
+        ("op", ctypes.c_int32),
+        ("precision", ctypes.c_int32),
+        ("sigma", ctypes.c_double),
+        ("amount", ctypes.c_double),
+        ("radius", ctypes.c_int32),
+        ("n_offsets", ctypes.c_int32),
+        ("offsets", ctypes.POINTER(ctypes.c_int32)),
+        ("n_weights", ctypes.c_int32),
+        ("weights", ctypes.POINTER(ctypes.c_float)),
+    ]
+
+
+class HbChunk(ctypes.Structure):
+    _fields_ = [
+        ("z_start", ctypes.c_int64),
+        ("z_stop", ctypes.c_int64),
+        ("halo_lo", ctypes.c_int64),
+        ("halo_hi", ctypes.c_int64),
+    ]
+
+
+CANCEL_FN = ctypes.CFUNCTYPE(ctypes.c_int32, ctypes.c_void_p)
+
+
+class HbExec(ctypes.Structure):
+    _fields_ = [
+        ("device", ctypes.c_int32),
+        ("pipeline_depth", ctypes.c_int32),
+        ("device_budget", ctypes.c_int64),
+        ("cancel", CANCEL_FN),
+        ("cancel_ctx", ctypes.c_void_p),
+        ("chunk_seconds", ctypes.POINTER(ctypes.c_double)),
+        ("fault_chunk", ctypes.c_int32),
+        ("host_threads", ctypes.c_int32),
+    ]
+
+
+class HbReport(ctypes.Structure):
+    _fields_ = [
+        ("chunk_count", ctypes.c_int64),
+        ("failed_chunk", ctypes.c_int64),
+        ("minimum_bytes", ctypes.c_int64),
+        ("device_peak_bytes", ctypes.c_int64),
+        ("device_residual_bytes", ctypes.c_int64),
+        ("h2d_bytes", ctypes.c_int64),
+        ("d2h_bytes", ctypes.c_int64),
+        ("h2d_ms", ctypes.c_double),
+        ("kernel_ms", ctypes.c_double),
+        ("d2h_ms", ctypes.c_double),
+        ("wall_ms", ctypes.c_double),
+        ("kernel_launches", ctypes.c_int64),
+        ("message", ctypes.c_char * 512),
+    ]
+
+
+# Every symbol include/harpia_b200.h declares (checked by tests/test_abi.py).
+EXPORTS = (
+    "hb_abi_version", "hb_version", "hb_device_info", "hb_device_count",
+    "hb_gaussian_radius", "hb_gaussian_weights", "hb_chain_halo", "hb_run",
+    "hb_apply_device", "hb_chain_out_dtype", "hb_trim_device",
+    "hb_device_pool_bytes", "hb_pin", "hb_unpin", "hb_last_error",
+)
+
+_lock = threading.Lock()
+_lib = None
+
+
+def load() -> ctypes.CDLL:
+    """Load the device library; raise loudly if it has not been built."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not LIB_PATH.exists():
+            raise RuntimeError(
+                f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+                " (there is no CPU fallback for the hot path)")
+        L = ctypes.CDLL(str(LIB_PATH))
+        i32, i64, vp, dbl = ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p, ctypes.c_double
+        L.hb_abi_version.restype = i32
+        L.hb_version.restype = ctypes.c_char_p
+        L.hb_last_error.restype = ctypes.c_char_p
+        L.hb_device_count.restype = i32
+        L.hb_device_info.argtypes = [i32, ctypes.POINTER(i64), ctypes.POINTER(i64)]
+        L.hb_device_info.restype = i32
+        L.hb_gaussian_radius.argtypes = [dbl]
+        L.hb_gaussian_radius.restype = i32
+        L.hb_gaussian_weights.argtypes = [dbl, ctypes.POINTER(ctypes.c_float), i32]
+        L.hb_gaussian_weights.restype = i32
+        L.hb_chain_halo.argtypes = [ctypes.POINTER(HbStage), i32]
+        L.hb_chain_halo.restype = i64
+        L.hb_chain_out_dtype.argtypes = [ctypes.POINTER(HbStage), i32, i32]
+        L.hb_chain_out_dtype.restype = i32
+        L.hb_run.argtypes = [ctypes.POINTER(HbVolume), ctypes.POINTER(HbVolume),
+                             ctypes.POINTER(HbStage), i32, ctypes.POINTER(HbChunk), i64,
+                             ctypes.POINTER(HbExec), ctypes.POINTER(HbReport)]
+        L.hb_run.restype = i32
+        L.hb_apply_device.argtypes = [ctypes.POINTER(HbVolume), ctypes.POINTER(HbVolume),
+                                      ctypes.POINTER(HbStage), i32, i64, vp, i32,
+                                      ctypes.POINTER(HbReport)]
+        L.hb_apply_device.restype = i32
+        L.hb_trim_device.argtypes = [i32]
+        L.hb_trim_device.restype = i32
+        L.hb_device_pool_bytes.argtypes = [i32]
+        L.hb_device_pool_bytes.restype = i64
+        L.hb_pin.argtypes = [vp, i64]
+        L.hb_pin.restype = i32
+        L.hb_unpin.argtypes = [vp]
+        L.hb_unpin.restype = i32
+        if L.hb_abi_version() != 1:
+            raise RuntimeError("libharpia_b200.so ABI version mismatch")
+        _lib = L
+        return L
+
+
+def device_count() -> int:
+    return int(load().hb_device_count())
+
+
+def device_info(dev: int = 0) -> tuple[int, int]:
+    f, t = ctypes.c_int64(0), ctypes.c_int64(0)
+    rc = load().hb_device_info(int(dev), ctypes.byref(f), ctypes.byref(t))
+    raise_for_status(rc, last_error())
+    return int(f.value), int(t.value)
+
+
+def last_error() -> str:
+    return (load().hb_last_error() or b"").decode(errors="replace")
+
+
+def current_device() -> int:
+    env = os.environ.get("HARPIA_DEVICE")
+    if env is not None:
+        return int(env)
+    return int(os.environ.get("LOCAL_RANK", "0"))
+
+
+# ---------------------------------------------------------------------------
+# Stage descriptions (Python side of hb_stage)
+# ---------------------------------------------------------------------------
+@dataclass
+class Stage:
+    op: int
+    precision: int = PREC_FAST
+    sigma: float = 0.0
+    amount: float = 0.0
+    radius: int = 0
+    offsets: Optional[np.ndarray] = None   # (n, 3) int32
+    weights: Optional[np.ndarray] = None   # float32 taps
+
+    def halo(self) -> int:
+        if self.op in (OP_GAUSSIAN, OP_UNSHARP):
+            return (len(self.weights) - 1) // 2
+        if self.op == OP_LOG:
+            return (len(self.weights) - 1) // 2 + 2
+        if self.op in (OP_MEAN, OP_MEDIAN):
+            return int(self.radius)
+        if self.op in (OP_ERODE, OP_DILATE):
+            return int(np.abs(self.offsets[:, 0]).max())
+        return 0
+
+    def out_dtype(self, in_dtype: np.dtype) -> np.dtype:
+        if self.op in (OP_GAUSSIAN, OP_UNSHARP, OP_LOG, OP_MEAN):
+            return np.dtype("float32")
+        return np.dtype(in_dtype)
+
+
+@dataclass
+class DeviceProgram:
+    """A map operator expressed as a chain of device stages (the unit the
+    native executor runs per chunk, replacing ``fn`` at chunking.py:257)."""
+
+    stages: list = field(default_factory=list)
+
+    def halo(self) -> int:
+        return int(sum(s.halo() for s in self.stages))
+
+    def out_dtype(self, in_dtype) -> np.dtype:
+        dt = np.dtype(in_dtype)
+        for s in self.stages:
+            dt = s.out_dtype(dt)
+        return dt
+
+
+class _Marshalled:
+    """Keeps the ctypes arrays alive for the duration of a native call."""
+
+    def __init__(self, program: DeviceProgram):
+        n = len(program.stages)
+        self.arr = (HbStage * n)()
+        self._keep = []
+        for i, s in enumerate(program.stages):
+            st = self.arr[i]
+            st.op = s.op
+            st.precision = s.precision
+            st.sigma = float(s.sigma)
+            st.amount = float(s.amount)
+            st.radius = int(s.radius)
+            if s.offsets is not None:
+                off = np.ascontiguousarray(s.offsets, dtype=np.int32).reshape(-1, 3)
+                self._keep.append(off)
+                st.n_offsets = off.shape[0]
+                st.offsets = off.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+            if s.weights is not None:
+                w = np.ascontiguousarray(s.weights, dtype=np.float32)
+                self._keep.append(w)
+                st.n_weights = w.size
+                st.weights = w.ctypes.data_as(ctypes.POINTER(ctypes.c_float))
+        self.n = n
+
+
+def _host_volume(a: np.ndarray) -> HbVolume:
+    return HbVolume(a.ctypes.data, DTYPE_CODE[a.dtype], HB_HOST, *a.shape)
+
+
+@dataclass
+class NativeReport:
+    chunk_count: int
+    chunk_seconds: list
+    device_peak_bytes: int
+    device_residual_bytes: int
+    h2d_bytes: int
+    d2h_bytes: int
+    kernel_seconds: float
+    wall_seconds: float
+    kernel_launches: int
+
+
+def run_host(data: np.ndarray, out: np.ndarray, program: DeviceProgram,
+             chunks: Sequence[tuple[int, int, int, int]], *, device: Optional[int] = None,
+             cancel: Optional[Callable[[], bool]] = None, device_budget: int = 0,
+             pipeline_depth: int = 0, fault_chunk: int = -1,
+             host_threads: int = 0) -> NativeReport:
+    """hb_run: stream host volume ``data`` through ``program`` chunk by chunk."""
+    L = load()
+    if data.dtype not in DTYPE_CODE or out.dtype not in DTYPE_CODE:
+        raise UnsupportedFormatError(f"unsupported dtype {data.dtype} -> {out.dtype}")
+    if not (data.flags.c_contiguous and out.flags.c_contiguous):
+        raise ParameterError("volumes must be C-contiguous (Z, Y, X)")
+    m = _Marshalled(program)
+    nch = len(chunks)
+    carr = (HbChunk * max(nch, 1))()
+    for i, c in enumerate(chunks):
+        carr[i] = HbChunk(*[int(v) for v in c])
+    secs = (ctypes.c_double * max(nch, 1))()
+    ex = HbExec()
+    ex.device = current_device() if device is None else int(device)
+    ex.pipeline_depth = int(pipeline_depth)
+    ex.device_budget = int(device_budget)
+    ex.fault_chunk = int(fault_chunk)
+    ex.host_threads = int(host_threads)
+    ex.chunk_seconds = ctypes.cast(secs, ctypes.POINTER(ctypes.c_double))
+    cb = None
+    if cancel is not None:
+        def _cb(_ctx):
+            try:
+                return 1 if cancel() else 0
+            except Exception:  # a failing cancel probe cancels the job
+                return 1
+        cb = CANCEL_FN(_cb)
+        ex.cancel = cb
+    vin, vout = _host_volume(data), _host_volume(out)
+    rep = HbReport()
+    rc = L.hb_run(ctypes.byref(vin), ctypes.byref(vout), m.arr, m.n, carr, nch,
+                  ctypes.byref(ex), ctypes.byref(rep))
+    if rc != HB_OK:
+        raise_for_status(rc, rep.message.decode(errors="replace"),
+                         failed_chunk=rep.failed_chunk, minimum_bytes=rep.minimum_bytes)
+    return NativeReport(
+        chunk_count=int(rep.chunk_count),
+        chunk_seconds=[float(secs[i]) for i in range(nch)],
+        device_peak_bytes=int(rep.device_peak_bytes),
+        device_residual_bytes=int(rep.device_residual_bytes),
+        h2d_bytes=int(rep.h2d_bytes),
+        d2h_bytes=int(rep.d2h_bytes),
+        kernel_seconds=float(rep.kernel_ms) * 1e-3,
+        wall_seconds=float(rep.wall_ms) * 1e-3,
+        kernel_launches=int(rep.kernel_launches),
+    )
+
+
+def apply_device(inp, out, program: DeviceProgram, z_begin: int = 0, stream=None,
+                 synchronize: bool = False) -> int:
+    """hb_apply_device on torch CUDA tensors (or anything exposing data_ptr()).
+
+    ``inp``: (Z, Y, X) contiguous CUDA tensor; ``out``: (Zo, Y, X) tensor that
+    receives block slices [z_begin, z_begin + Zo).  Returns the number of kernel
+    launches enqueued.  Runs on ``stream`` (torch.cuda.Stream or raw handle;
+    default: torch's current stream)."""
+    import torch
+
+    L = load()
+    code_in = DTYPE_CODE.get(np.dtype(str(inp.dtype).replace("torch.", "")))
+    code_out = DTYPE_CODE.get(np.dtype(str(out.dtype).replace("torch.", "")))
+    if code_in is None or code_out is None:
+        raise UnsupportedFormatError(f"unsupported tensor dtype {inp.dtype} -> {out.dtype}")
+    if not (inp.is_contiguous() and out.is_contiguous()):
+        raise ParameterError("device blocks must be contiguous")
+    m = _Marshalled(program)
+    vin = HbVolume(inp.data_ptr(), code_in, HB_DEVICE, *inp.shape)
+    vout = HbVolume(out.data_ptr(), code_out, HB_DEVICE, *out.shape)
+    if stream is None:
+        stream = torch.cuda.current_stream(inp.device)
+    handle = stream.cuda_stream if hasattr(stream, "cuda_stream") else stream
+    rep = HbReport()
+    rc = L.hb_apply_device(ctypes.byref(vin), ctypes.byref(vout), m.arr, m.n, int(z_begin),
+                           ctypes.c_void_p(handle), 1 if synchronize else 0, ctypes.byref(rep))
+    if rc != HB_OK:
+        raise_for_status(rc, rep.message.decode(errors="replace"),
+                         failed_chunk=rep.failed_chunk, minimum_bytes=rep.minimum_bytes)
+    return int(rep.kernel_launches)
+
+
+def trim_device(dev: Optional[int] = None) -> None:
+    load().hb_trim_device(current_device() if dev is None else int(dev))
+
+
+def device_pool_bytes(dev: Optional[int] = None) -> int:
+    return int(load().hb_device_pool_bytes(current_device() if dev is None else int(dev)))

@@ -1,0 +1,941 @@
+// executor.cu — C ABI (include/harpia_b200.h): stage-chain planning, the device
+// memory manager, and the chunked streaming executor that replaces
+// chunking.execute_chunked (chunking.py:215-279) for map operators.
+//
+// Memory model (SURVEY.md §5 "Memory release"): every device byte a job uses
+// comes from a library-private cudaMemPool per device; at the end of every
+// synchronous job the pool is trimmed to zero, so the job's device residual is
+// exactly 0 and PyTorch's caching allocator is never involved.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "ops.cuh"
+
+using namespace hb;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+void set_err(hb_report* rep, const std::string& m) {
+  g_last_error = m;
+  if (rep) {
+    std::snprintf(rep->message, sizeof(rep->message), "%s", m.c_str());
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Stage normalisation
+// ---------------------------------------------------------------------------
+struct StageDesc {
+  int op = HB_OP_IDENTITY;
+  int precision = HB_PREC_FAST;
+  int64_t halo = 0;
+  int radius = 0;
+  float amount = 0.f;
+  Taps taps{};
+  std::vector<int32_t> offsets;  // reflected for dilation
+  int in_dt = HB_F32, out_dt = HB_F32;
+};
+
+int gaussian_radius(double sigma) { return (int)std::ceil(4.0 * sigma); }
+
+// numpy pairwise_sum for n <= 128 (see oracle/harpia_oracle.c for the citation)
+double pairwise_sum(const double* a, int n) {
+  if (n < 8) {
+    double r = 0.;
+    for (int i = 0; i < n; i++) r += a[i];
+    return r;
+  }
+  double r[8];
+  int i;
+  for (i = 0; i < 8; i++) r[i] = a[i];
+  for (i = 8; i < n - (n % 8); i += 8)
+    for (int j = 0; j < 8; j++) r[j] += a[i + j];
+  double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+  for (; i < n; i++) res += a[i];
+  return res;
+}
+
+int fill_weights(double sigma, float* out, int cap) {
+  int r = gaussian_radius(sigma);
+  int n = 2 * r + 1;
+  if (n > cap) return -1;
+  std::vector<double> k(n);
+  for (int i = 0; i < n; i++) {
+    double q = (double)(i - r) / sigma;
+    k[i] = std::exp(-0.5 * (q * q));
+  }
+  double s = pairwise_sum(k.data(), n);
+  for (int i = 0; i < n; i++) out[i] = (float)(k[i] / s);
+  return n;
+}
+
+int z_extent(const std::vector<int32_t>& off) {
+  int e = 0;
+  for (size_t k = 0; k < off.size(); k += 3) e = std::max(e, std::abs(off[k]));
+  return e;
+}
+
+hb_status normalise(const hb_stage* st, int nst, int in_dt, std::vector<StageDesc>& out,
+                    std::string& msg) {
+  if (nst < 1) {
+    msg = "empty stage chain";
+    return HB_EPARAM;
+  }
+  int dt = in_dt;
+  for (int i = 0; i < nst; i++) {
+    const hb_stage& s = st[i];
+    StageDesc d;
+    d.op = s.op;
+    d.precision = s.precision;
+    d.in_dt = dt;
+    switch (s.op) {
+      case HB_OP_IDENTITY:
+        d.out_dt = dt;
+        break;
+      case HB_OP_GAUSSIAN:
+      case HB_OP_UNSHARP:
+      case HB_OP_LOG: {
+        if (!(s.sigma > 0) || !std::isfinite(s.sigma)) {
+          msg = "sigma must be positive, got " + std::to_string(s.sigma);
+          return HB_EPARAM;
+        }
+        int r = gaussian_radius(s.sigma);
+        if (2 * r + 1 > kMaxTaps) {
+          msg = "sigma too large for the device stencil (ceil(4 sigma) must be <= 64)";
+          return HB_EUNSUPPORTED;
+        }
+        d.taps.R = r;
+        if (s.weights && s.n_weights > 0) {
+          if (s.n_weights != 2 * r + 1) {
+            msg = "weights length does not match 2*ceil(4*sigma)+1";
+            return HB_EPARAM;
+          }
+          std::memcpy(d.taps.w, s.weights, sizeof(float) * s.n_weights);
+        } else {
+          fill_weights(s.sigma, d.taps.w, kMaxTaps);
+        }
+        for (int k = 1; k <= r; k++)
+          if (d.taps.w[r + k] != d.taps.w[r - k]) {
+            msg = "gaussian weights must be symmetric";
+            return HB_EPARAM;
+          }
+        d.halo = r + (s.op == HB_OP_LOG ? 2 : 0);
+        d.amount = (float)s.amount;
+        if (s.op == HB_OP_LOG) d.precision = s.precision;  // exact recommended
+        d.out_dt = HB_F32;
+        break;
+      }
+      case HB_OP_MEAN:
+      case HB_OP_MEDIAN:
+        if (s.radius < 1) {
+          msg = "radius must be >= 1, got " + std::to_string(s.radius);
+          return HB_EPARAM;
+        }
+        if (s.radius > 50) {
+          msg = "radius too large";
+          return HB_EUNSUPPORTED;
+        }
+        d.radius = s.radius;
+        d.halo = s.radius;
+        d.out_dt = s.op == HB_OP_MEAN ? HB_F32 : dt;
+        break;
+      case HB_OP_ERODE:
+      case HB_OP_DILATE: {
+        if (s.n_offsets < 1 || !s.offsets) {
+          msg = "structuring element must not be empty";
+          return HB_EPARAM;
+        }
+        bool has_origin = false;
+        d.offsets.resize(3 * (size_t)s.n_offsets);
+        int sgn = s.op == HB_OP_DILATE ? -1 : 1;  // dilate uses the reflected SE
+        for (int k = 0; k < s.n_offsets; k++) {
+          int dz = s.offsets[3 * k], dy = s.offsets[3 * k + 1], dx = s.offsets[3 * k + 2];
+          if (dz == 0 && dy == 0 && dx == 0) has_origin = true;
+          d.offsets[3 * k] = sgn * dz;
+          d.offsets[3 * k + 1] = sgn * dy;
+          d.offsets[3 * k + 2] = sgn * dx;
+        }
+        if (!has_origin) {
+          msg = "structuring element must contain the origin";
+          return HB_EPARAM;
+        }
+        d.halo = z_extent(d.offsets);
+        d.out_dt = dt;
+        break;
+      }
+      default:
+        msg = "unknown operator code " + std::to_string(s.op);
+        return HB_EPARAM;
+    }
+    dt = d.out_dt;
+    out.push_back(std::move(d));
+  }
+  return HB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Device memory: private pool per device, trimmed to zero after each job.
+// ---------------------------------------------------------------------------
+struct DeviceCtx {
+  std::mutex mu;
+  cudaMemPool_t pool = nullptr;
+  bool init = false;
+};
+DeviceCtx g_dev[64];
+
+cudaError_t ensure_pool(int dev) {
+  DeviceCtx& d = g_dev[dev];
+  if (d.init) return cudaSuccess;
+  cudaMemPoolProps props{};
+  props.allocType = cudaMemAllocationTypePinned;
+  props.location.type = cudaMemLocationTypeDevice;
+  props.location.id = dev;
+  cudaError_t e = cudaMemPoolCreate(&d.pool, &props);
+  if (e != cudaSuccess) return e;
+  uint64_t keep = UINT64_MAX;  // hold memory between async calls; jobs trim explicitly
+  cudaMemPoolSetAttribute(d.pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  d.init = true;
+  return cudaSuccess;
+}
+
+void pool_reset_peak(int dev) {
+  uint64_t z = 0;
+  cudaMemPoolSetAttribute(g_dev[dev].pool, cudaMemPoolAttrUsedMemHigh, &z);
+  cudaMemPoolSetAttribute(g_dev[dev].pool, cudaMemPoolAttrReservedMemHigh, &z);
+}
+int64_t pool_attr(int dev, cudaMemPoolAttr a) {
+  uint64_t v = 0;
+  cudaMemPoolGetAttribute(g_dev[dev].pool, a, &v);
+  return (int64_t)v;
+}
+
+struct PoolAlloc {
+  cudaMemPool_t pool;
+  cudaStream_t s;
+  std::vector<void*> ptrs;
+  cudaError_t err = cudaSuccess;
+  void* get(size_t bytes) {
+    if (bytes == 0) bytes = 256;
+    void* p = nullptr;
+    cudaError_t e = cudaMallocFromPoolAsync(&p, bytes, pool, s);
+    if (e != cudaSuccess) {
+      err = e;
+      return nullptr;
+    }
+    ptrs.push_back(p);
+    return p;
+  }
+  void release() {
+    for (void* p : ptrs) cudaFreeAsync(p, s);
+    ptrs.clear();
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Chain evaluation on a device block
+// ---------------------------------------------------------------------------
+struct Range {
+  int64_t a, b;  // [a, b) in block-local z
+};
+
+// Output range each stage must produce so that the last stage can produce
+// [zo, zo+nzo): stage s covers [zo - H_s, zo + nzo + H_s) ∩ [0, nz) where H_s
+// is the sum of the halos of the stages after s.
+std::vector<Range> stage_ranges(const std::vector<StageDesc>& st, int64_t nz, int64_t zo,
+                                int64_t nzo) {
+  std::vector<Range> r(st.size());
+  int64_t h = 0;
+  for (int s = (int)st.size() - 1; s >= 0; --s) {
+    r[s].a = std::max<int64_t>(0, zo - h);
+    r[s].b = std::min<int64_t>(nz, zo + nzo + h);
+    h += st[s].halo;
+  }
+  return r;
+}
+
+// Scratch bytes needed to evaluate the chain (excluding the final output).
+size_t chain_scratch(const std::vector<StageDesc>& st, int64_t nz, int64_t ny, int64_t nx,
+                     int64_t zo, int64_t nzo) {
+  auto rg = stage_ranges(st, nz, zo, nzo);
+  size_t plane = (size_t)ny * nx, total = 0;
+  for (size_t s = 0; s < st.size(); ++s) {
+    size_t n = (size_t)(rg[s].b - rg[s].a);
+    if (s + 1 < st.size()) total += n * plane * dtype_size(st[s].out_dt);  // stage output
+    // per-op temporaries (generic gaussian: one f32 buffer; LoG: g + tmp)
+    if (st[s].op == HB_OP_GAUSSIAN || st[s].op == HB_OP_UNSHARP || st[s].op == HB_OP_MEAN)
+      total += n * plane * 4;
+    if (st[s].op == HB_OP_LOG) {
+      int64_t in_n = s == 0 ? nz : (rg[s - 1].b - rg[s - 1].a);
+      size_t gn = (size_t)std::min<int64_t>(in_n, n + 4);
+      total += 2 * gn * plane * 4;
+    }
+  }
+  return total + 4096 * st.size();
+}
+
+cudaError_t run_stage(const StageDesc& d, const DevIn& in, int64_t zo, int64_t nzo, void* out,
+                      PoolAlloc& pa, cudaStream_t s, int64_t* launches) {
+  const size_t plane = (size_t)in.ny * in.nx;
+  switch (d.op) {
+    case HB_OP_IDENTITY:
+      return copy_slices(in, zo, nzo, out, s, launches);
+    case HB_OP_GAUSSIAN:
+    case HB_OP_UNSHARP: {
+      EpiArgs epi;
+      if (d.op == HB_OP_UNSHARP) {
+        epi.kind = EPI_UNSHARP;
+        epi.orig = in.p;
+        epi.orig_dt = in.dt;
+        epi.orig_zo = zo;
+        epi.amount = d.amount;
+      }
+      if (d.precision == HB_PREC_FAST) {
+        cudaError_t e = gaussian_fused(in, zo, nzo, (float*)out, d.taps, epi, s, launches);
+        if (e != cudaErrorNotSupported) return e;
+        cudaGetLastError();  // clear the NotSupported marker
+      }
+      float* tmp = (float*)pa.get((size_t)nzo * plane * 4);
+      if (!tmp) return pa.err;
+      return gaussian_generic(in, zo, nzo, (float*)out, d.taps,
+                              d.precision == HB_PREC_EXACT, epi, tmp, s, launches);
+    }
+    case HB_OP_MEAN: {
+      float* tmp = (float*)pa.get((size_t)nzo * plane * 4);
+      if (!tmp) return pa.err;
+      return mean_generic(in, zo, nzo, (float*)out, d.radius, tmp, s, launches);
+    }
+    case HB_OP_LOG: {
+      // smoothed g over [zo-2, zo+nzo+2) ∩ [0, nz) then the cd∘cd stage
+      int64_t g0 = std::max<int64_t>(0, zo - 2), g1 = std::min<int64_t>(in.nz, zo + nzo + 2);
+      float* g = (float*)pa.get((size_t)(g1 - g0) * plane * 4);
+      float* tmp = (float*)pa.get((size_t)(g1 - g0) * plane * 4);
+      if (!g || !tmp) return pa.err;
+      EpiArgs none;
+      cudaError_t e = cudaSuccess;
+      if (d.precision == HB_PREC_FAST) {
+        e = gaussian_fused(in, g0, g1 - g0, g, d.taps, none, s, launches);
+        if (e == cudaErrorNotSupported) {
+          cudaGetLastError();
+          e = gaussian_generic(in, g0, g1 - g0, g, d.taps, false, none, tmp, s, launches);
+        }
+      } else {
+        e = gaussian_generic(in, g0, g1 - g0, g, d.taps, true, none, tmp, s, launches);
+      }
+      if (e != cudaSuccess) return e;
+      return log_diff(g, g0, g1 - g0, in.nz, in.ny, in.nx, zo, nzo, (float*)out, s, launches);
+    }
+    case HB_OP_MEDIAN:
+      return median(in, zo, nzo, out, d.radius, s, launches);
+    case HB_OP_ERODE:
+    case HB_OP_DILATE:
+      return morph(in, zo, nzo, out, d.offsets.data(), (int)(d.offsets.size() / 3),
+                   d.op == HB_OP_DILATE, s, launches);
+  }
+  return cudaErrorInvalidValue;
+}
+
+// Evaluate the chain on block `in`, writing [zo, zo+nzo) into `out`.
+cudaError_t run_chain(const std::vector<StageDesc>& st, const DevIn& in, int64_t zo,
+                      int64_t nzo, void* out, PoolAlloc& pa, cudaStream_t s,
+                      int64_t* launches) {
+  auto rg = stage_ranges(st, in.nz, zo, nzo);
+  DevIn cur = in;
+  int64_t cur_a = 0;  // block-local z of cur's slice 0
+  const size_t plane = (size_t)in.ny * in.nx;
+  for (size_t k = 0; k < st.size(); ++k) {
+    const bool last = k + 1 == st.size();
+    void* dst;
+    if (last) {
+      dst = out;
+    } else {
+      dst = pa.get((size_t)(rg[k].b - rg[k].a) * plane * dtype_size(st[k].out_dt));
+      if (!dst) return pa.err;
+    }
+    // in cur-local coordinates
+    int64_t lzo = rg[k].a - cur_a;
+    cudaError_t e = run_stage(st[k], cur, lzo, rg[k].b - rg[k].a, dst, pa, s, launches);
+    if (e != cudaSuccess) return e;
+    if (!last) {
+      cur.p = dst;
+      cur.dt = st[k].out_dt;
+      cur.nz = rg[k].b - rg[k].a;
+      cur_a = rg[k].a;
+    }
+  }
+  return cudaSuccess;
+}
+
+// ---------------------------------------------------------------------------
+// Host staging: parallel memcpy + cached pinned bounce ring
+// ---------------------------------------------------------------------------
+void par_memcpy(void* dst, const void* src, size_t bytes, int threads) {
+  if (bytes < (8u << 20) || threads <= 1) {
+    std::memcpy(dst, src, bytes);
+    return;
+  }
+  std::vector<std::thread> th;
+  size_t per = (bytes + threads - 1) / threads;
+  per = (per + 4095) & ~(size_t)4095;
+  for (int t = 0; t < threads; t++) {
+    size_t o = (size_t)t * per;
+    if (o >= bytes) break;
+    size_t n = std::min(per, bytes - o);
+    th.emplace_back([=] { std::memcpy((char*)dst + o, (const char*)src + o, n); });
+  }
+  for (auto& t : th) t.join();
+}
+
+struct PinnedRing {
+  static constexpr int kSlots = 4;
+  static constexpr size_t kPiece = 64u << 20;
+  void* buf[kSlots] = {};
+  cudaEvent_t ev[kSlots] = {};
+  bool used[kSlots] = {};
+  int next = 0;
+  bool ok = false;
+  cudaError_t init() {
+    if (ok) return cudaSuccess;
+    for (int i = 0; i < kSlots; i++) {
+      cudaError_t e = cudaMallocHost(&buf[i], kPiece);
+      if (e != cudaSuccess) return e;
+      cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming);
+    }
+    ok = true;
+    return cudaSuccess;
+  }
+};
+PinnedRing g_ring[64];
+
+bool is_pinned(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+// H2D of `bytes` from pageable host memory through the pinned ring.
+cudaError_t h2d_staged(PinnedRing& ring, void* dst, const void* src, size_t bytes,
+                       cudaStream_t s, int threads) {
+  size_t off = 0;
+  while (off < bytes) {
+    int i = ring.next;
+    ring.next = (ring.next + 1) % PinnedRing::kSlots;
+    if (ring.used[i]) cudaEventSynchronize(ring.ev[i]);
+    size_t n = std::min(PinnedRing::kPiece, bytes - off);
+    par_memcpy(ring.buf[i], (const char*)src + off, n, threads);
+    cudaError_t e = cudaMemcpyAsync((char*)dst + off, ring.buf[i], n, cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return e;
+    cudaEventRecord(ring.ev[i], s);
+    ring.used[i] = true;
+    off += n;
+  }
+  return cudaSuccess;
+}
+
+// D2H into pageable host memory through the pinned ring (synchronous for the
+// host thread; `s` must already be ordered after the producing work).
+cudaError_t d2h_staged(PinnedRing& ring, void* dst, const void* src, size_t bytes,
+                       cudaStream_t s, int threads) {
+  struct Pending { int slot; size_t off, n; };
+  std::vector<Pending> q;
+  size_t off = 0;
+  auto drain_one = [&]() {
+    Pending p = q.front();
+    q.erase(q.begin());
+    cudaEventSynchronize(ring.ev[p.slot]);
+    par_memcpy((char*)dst + p.off, ring.buf[p.slot], p.n, threads);
+    ring.used[p.slot] = false;
+  };
+  while (off < bytes) {
+    if ((int)q.size() >= PinnedRing::kSlots - 1) drain_one();
+    int i = ring.next;
+    ring.next = (ring.next + 1) % PinnedRing::kSlots;
+    if (ring.used[i]) cudaEventSynchronize(ring.ev[i]);
+    size_t n = std::min(PinnedRing::kPiece, bytes - off);
+    cudaError_t e = cudaMemcpyAsync(ring.buf[i], (const char*)src + off, n, cudaMemcpyDeviceToHost, s);
+    if (e != cudaSuccess) return e;
+    cudaEventRecord(ring.ev[i], s);
+    ring.used[i] = true;
+    q.push_back({i, off, n});
+    off += n;
+  }
+  while (!q.empty()) drain_one();
+  return cudaSuccess;
+}
+
+int auto_threads(int req) {
+  if (req > 0) return req;
+  unsigned n = std::thread::hardware_concurrency();
+  return (int)std::max(1u, std::min(8u, n ? n / 2 : 1u));
+}
+
+double now_ms() {
+  return std::chrono::duration<double, std::milli>(
+             std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+int32_t hb_abi_version(void) { return HB_ABI_VERSION; }
+
+const char* hb_version(void) { return "harpia-b200 0.1.0 (sm_100a)"; }
+
+const char* hb_last_error(void) { return g_last_error.c_str(); }
+
+int32_t hb_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+int32_t hb_device_info(int32_t dev, int64_t* free_bytes, int64_t* total_bytes) {
+  int n = hb_device_count();
+  if (dev < 0 || dev >= n) {
+    set_err(nullptr, "no CUDA device " + std::to_string(dev));
+    return HB_EBUDGET_UNAVAILABLE;
+  }
+  cudaSetDevice(dev);
+  size_t f = 0, t = 0;
+  cudaError_t e = cudaMemGetInfo(&f, &t);
+  if (e != cudaSuccess) {
+    set_err(nullptr, cudaGetErrorString(e));
+    return HB_EBUDGET_UNAVAILABLE;
+  }
+  if (free_bytes) *free_bytes = (int64_t)f;
+  if (total_bytes) *total_bytes = (int64_t)t;
+  return HB_OK;
+}
+
+int32_t hb_gaussian_radius(double sigma) { return gaussian_radius(sigma); }
+
+int32_t hb_gaussian_weights(double sigma, float* out, int32_t capacity) {
+  if (!(sigma > 0)) return -1;
+  return fill_weights(sigma, out, capacity);
+}
+
+int64_t hb_chain_halo(const hb_stage* stages, int32_t nstages) {
+  std::vector<StageDesc> st;
+  std::string msg;
+  if (normalise(stages, nstages, HB_F32, st, msg) != HB_OK) return -1;
+  int64_t h = 0;
+  for (auto& d : st) h += d.halo;
+  return h;
+}
+
+int32_t hb_chain_out_dtype(const hb_stage* stages, int32_t nstages, int32_t in_dtype) {
+  std::vector<StageDesc> st;
+  std::string msg;
+  if (in_dtype < HB_U8 || in_dtype > HB_F32) return -1;
+  if (normalise(stages, nstages, in_dtype, st, msg) != HB_OK) return -1;
+  return st.back().out_dt;
+}
+
+int32_t hb_pin(void* ptr, int64_t bytes) {
+  cudaError_t e = cudaHostRegister(ptr, (size_t)bytes, cudaHostRegisterDefault);
+  if (e != cudaSuccess) {
+    set_err(nullptr, cudaGetErrorString(e));
+    cudaGetLastError();
+    return HB_ECUDA;
+  }
+  return HB_OK;
+}
+
+int32_t hb_unpin(void* ptr) {
+  cudaError_t e = cudaHostUnregister(ptr);
+  if (e != cudaSuccess) {
+    set_err(nullptr, cudaGetErrorString(e));
+    cudaGetLastError();
+    return HB_ECUDA;
+  }
+  return HB_OK;
+}
+
+int32_t hb_trim_device(int32_t dev) {
+  if (dev < 0 || dev >= hb_device_count()) return HB_EPARAM;
+  std::lock_guard<std::mutex> lk(g_dev[dev].mu);
+  if (!g_dev[dev].init) return HB_OK;
+  cudaSetDevice(dev);
+  cudaDeviceSynchronize();
+  cudaMemPoolTrimTo(g_dev[dev].pool, 0);
+  return HB_OK;
+}
+
+int64_t hb_device_pool_bytes(int32_t dev) {
+  if (dev < 0 || dev >= 64 || !g_dev[dev].init) return 0;
+  return pool_attr(dev, cudaMemPoolAttrReservedMemCurrent);
+}
+
+int32_t hb_apply_device(const hb_volume* in, hb_volume* out, const hb_stage* stages,
+                        int32_t nstages, int64_t z_begin, void* stream, int32_t synchronize,
+                        hb_report* rep) {
+  if (rep) {
+    std::memset(rep, 0, sizeof(*rep));
+    rep->failed_chunk = -1;
+    rep->chunk_count = 1;
+  }
+  if (!in || !out || !in->data || !out->data || in->location != HB_DEVICE ||
+      out->location != HB_DEVICE) {
+    set_err(rep, "hb_apply_device needs device volumes");
+    return HB_EPARAM;
+  }
+  if (in->nz < 1 || in->ny < 1 || in->nx < 1 || out->ny != in->ny || out->nx != in->nx ||
+      z_begin < 0 || out->nz < 0 || z_begin + out->nz > in->nz) {
+    set_err(rep, "shape mismatch between device blocks");
+    return HB_EPARAM;
+  }
+  std::vector<StageDesc> st;
+  std::string msg;
+  hb_status rc = normalise(stages, nstages, in->dtype, st, msg);
+  if (rc != HB_OK) {
+    set_err(rep, msg);
+    return rc;
+  }
+  if (st.back().out_dt != out->dtype) {
+    set_err(rep, "output dtype does not match the chain's output dtype");
+    return HB_EPARAM;
+  }
+  int dev = 0;
+  cudaPointerAttributes pa_attr;
+  if (cudaPointerGetAttributes(&pa_attr, in->data) == cudaSuccess && pa_attr.device >= 0)
+    dev = pa_attr.device;
+  cudaGetLastError();
+  cudaSetDevice(dev);
+  std::lock_guard<std::mutex> lk(g_dev[dev].mu);
+  cudaError_t e = ensure_pool(dev);
+  if (e != cudaSuccess) {
+    set_err(rep, std::string("device pool: ") + cudaGetErrorString(e));
+    return HB_ECUDA;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  if (synchronize) pool_reset_peak(dev);
+  PoolAlloc pa{g_dev[dev].pool, s};
+  DevIn din{in->data, in->dtype, in->nz, in->ny, in->nx};
+  int64_t launches = 0;
+  double t0 = now_ms();
+  e = run_chain(st, din, z_begin, out->nz, out->data, pa, s, &launches);
+  pa.release();
+  if (rep) rep->kernel_launches = launches;
+  if (e != cudaSuccess) {
+    cudaStreamSynchronize(s);
+    cudaGetLastError();
+    cudaMemPoolTrimTo(g_dev[dev].pool, 0);
+    set_err(rep, std::string("CUDA: ") + cudaGetErrorString(e));
+    if (rep) rep->failed_chunk = 0;
+    return HB_ECUDA;
+  }
+  if (synchronize) {
+    e = cudaStreamSynchronize(s);
+    if (rep) {
+      rep->device_peak_bytes = pool_attr(dev, cudaMemPoolAttrUsedMemHigh);
+      rep->wall_ms = now_ms() - t0;
+    }
+    cudaMemPoolTrimTo(g_dev[dev].pool, 0);
+    if (rep) rep->device_residual_bytes = pool_attr(dev, cudaMemPoolAttrReservedMemCurrent);
+    if (e != cudaSuccess) {
+      set_err(rep, std::string("CUDA: ") + cudaGetErrorString(e));
+      cudaGetLastError();
+      if (rep) rep->failed_chunk = 0;
+      return HB_ECUDA;
+    }
+  }
+  return HB_OK;
+}
+
+int32_t hb_run(const hb_volume* in, hb_volume* out, const hb_stage* stages, int32_t nstages,
+               const hb_chunk* chunks, int64_t nchunks, const hb_exec* ex, hb_report* rep) {
+  hb_report dummy;
+  if (!rep) rep = &dummy;
+  std::memset(rep, 0, sizeof(*rep));
+  rep->failed_chunk = -1;
+  const double t_start = now_ms();
+  if (!in || !out || !in->data || !out->data || !ex || !chunks) {
+    set_err(rep, "null argument");
+    return HB_EPARAM;
+  }
+  if (in->location != HB_HOST || out->location != HB_HOST) {
+    set_err(rep, "hb_run streams host volumes; use hb_apply_device for device blocks");
+    return HB_EPARAM;
+  }
+  if (in->nz < 1 || in->ny < 1 || in->nx < 1 || out->nz != in->nz || out->ny != in->ny ||
+      out->nx != in->nx) {
+    set_err(rep, "input/output shapes differ");
+    return HB_EPARAM;
+  }
+  std::vector<StageDesc> st;
+  std::string msg;
+  hb_status rc = normalise(stages, nstages, in->dtype, st, msg);
+  if (rc != HB_OK) {
+    set_err(rep, msg);
+    return rc;
+  }
+  if (st.back().out_dt != out->dtype) {
+    set_err(rep, "output dtype does not match the chain's output dtype");
+    return HB_EPARAM;
+  }
+  // validate the plan: interiors must partition [0, Z), halos within the volume
+  int64_t expect = 0;
+  int64_t max_pad = 0, max_int = 0;
+  for (int64_t k = 0; k < nchunks; k++) {
+    const hb_chunk& c = chunks[k];
+    if (c.z_start != expect || c.z_stop <= c.z_start || c.halo_lo < 0 || c.halo_hi < 0 ||
+        c.z_start - c.halo_lo < 0 || c.z_stop + c.halo_hi > in->nz) {
+      set_err(rep, "invalid chunk plan at chunk " + std::to_string(k));
+      return HB_EPARAM;
+    }
+    expect = c.z_stop;
+    max_pad = std::max(max_pad, c.z_stop - c.z_start + c.halo_lo + c.halo_hi);
+    max_int = std::max(max_int, c.z_stop - c.z_start);
+  }
+  if (expect != in->nz) {
+    set_err(rep, "chunk interiors do not cover the volume");
+    return HB_EPARAM;
+  }
+  const int dev = ex->device;
+  if (dev < 0 || dev >= hb_device_count()) {
+    set_err(rep, "no CUDA device " + std::to_string(dev));
+    return HB_EBUDGET_UNAVAILABLE;
+  }
+  cudaSetDevice(dev);
+  std::lock_guard<std::mutex> lk(g_dev[dev].mu);
+  cudaError_t e = ensure_pool(dev);
+  if (e != cudaSuccess) {
+    set_err(rep, std::string("device pool: ") + cudaGetErrorString(e));
+    return HB_ECUDA;
+  }
+  const size_t plane = (size_t)in->ny * in->nx;
+  const size_t in_es = dtype_size(in->dtype), out_es = dtype_size(out->dtype);
+  // worst-case per-slot device bytes: padded input slab + interior output + chain scratch
+  size_t scratch = 0;
+  for (int64_t k = 0; k < nchunks; k++) {
+    const hb_chunk& c = chunks[k];
+    int64_t pn = c.z_stop - c.z_start + c.halo_lo + c.halo_hi;
+    scratch = std::max(scratch, chain_scratch(st, pn, in->ny, in->nx, c.halo_lo,
+                                              c.z_stop - c.z_start));
+  }
+  const size_t slot_bytes = (size_t)max_pad * plane * in_es + (size_t)max_int * plane * out_es + scratch;
+  int depth = ex->pipeline_depth > 0 ? ex->pipeline_depth : 2;
+  depth = (int)std::min<int64_t>(depth, std::max<int64_t>(1, nchunks));
+  size_t free_b = 0, total_b = 0;
+  cudaMemGetInfo(&free_b, &total_b);
+  // Hard limit: physically free device memory.  Soft target: the job budget
+  // (the planner's scratch factors are the reference's host estimates, so a
+  // plan the reference accepts must never fail here just because the device
+  // layout differs; we drop to a serial pipeline first).
+  size_t cap = free_b > (256u << 20) ? free_b - (256u << 20) : 0;
+  size_t soft = cap;
+  if (ex->device_budget > 0) soft = std::min(cap, (size_t)ex->device_budget);
+  while (depth > 1 && (size_t)depth * slot_bytes > soft) depth--;
+  if (slot_bytes > cap) {
+    rep->minimum_bytes = (int64_t)slot_bytes;
+    set_err(rep, "device budget of " + std::to_string(cap) + " bytes cannot hold one chunk (" +
+                     std::to_string(slot_bytes) + " bytes needed)");
+    return HB_EBUDGET_SMALL;
+  }
+  const int threads = auto_threads(ex->host_threads);
+  const bool in_pinned = is_pinned(in->data), out_pinned = is_pinned(out->data);
+  PinnedRing& ring = g_ring[dev];
+  if (!in_pinned || !out_pinned) {
+    e = ring.init();
+    if (e != cudaSuccess) {
+      set_err(rep, std::string("pinned staging: ") + cudaGetErrorString(e));
+      return HB_ECUDA;
+    }
+  }
+
+  cudaStream_t s_in, s_comp, s_out;
+  cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking);
+  cudaStreamCreateWithFlags(&s_comp, cudaStreamNonBlocking);
+  cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking);
+  std::vector<cudaEvent_t> ev_h2d(depth), ev_comp(depth), ev_d2h(depth), ev_k0(depth);
+  for (int i = 0; i < depth; i++) {
+    cudaEventCreate(&ev_h2d[i]);
+    cudaEventCreate(&ev_comp[i]);
+    cudaEventCreate(&ev_d2h[i]);
+    cudaEventCreate(&ev_k0[i]);
+  }
+  std::vector<cudaEvent_t> ev_done(nchunks);
+  for (auto& v : ev_done) cudaEventCreate(&v);
+  cudaEvent_t ev_start;
+  cudaEventCreate(&ev_start);
+
+  pool_reset_peak(dev);
+  std::vector<PoolAlloc> slots;
+  std::vector<void*> dbuf_in(depth), dbuf_out(depth);
+  for (int i = 0; i < depth; i++) {
+    slots.push_back(PoolAlloc{g_dev[dev].pool, s_comp});
+  }
+  PoolAlloc io{g_dev[dev].pool, s_comp};
+  for (int i = 0; i < depth && e == cudaSuccess; i++) {
+    dbuf_in[i] = io.get((size_t)max_pad * plane * in_es);
+    dbuf_out[i] = io.get((size_t)max_int * plane * out_es);
+    if (!dbuf_in[i] || !dbuf_out[i]) e = io.err;
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s_comp);
+  if (e != cudaSuccess) {
+    io.release();
+    cudaStreamSynchronize(s_comp);
+    cudaGetLastError();
+    cudaMemPoolTrimTo(g_dev[dev].pool, 0);
+    rep->minimum_bytes = (int64_t)slot_bytes;
+    set_err(rep, std::string("device allocation failed: ") + cudaGetErrorString(e));
+    return HB_EBUDGET_SMALL;
+  }
+
+  hb_status status = HB_OK;
+  int64_t launches = 0;
+  double kernel_ms = 0;
+  std::vector<int64_t> slot_chunk(depth, -1);
+  cudaEventRecord(ev_start, s_in);
+
+  // finish chunk k: its D2H into pageable memory (if needed) and bookkeeping
+  auto finish = [&](int64_t k) -> cudaError_t {
+    int slot = (int)(k % depth);
+    const hb_chunk& c = chunks[k];
+    int64_t n = c.z_stop - c.z_start;
+    size_t bytes = (size_t)n * plane * out_es;
+    char* host_dst = (char*)out->data + (size_t)c.z_start * plane * out_es;
+    cudaError_t err = cudaSuccess;
+    if (!out_pinned) {
+      cudaStreamWaitEvent(s_out, ev_comp[slot], 0);
+      err = d2h_staged(ring, host_dst, dbuf_out[slot], bytes, s_out, threads);
+      cudaEventRecord(ev_d2h[slot], s_out);
+      cudaEventRecord(ev_done[k], s_out);
+    }
+    cudaEventSynchronize(ev_done[k]);
+    float ms = 0;
+    if (cudaEventElapsedTime(&ms, ev_k0[slot], ev_comp[slot]) == cudaSuccess) kernel_ms += ms;
+    rep->d2h_bytes += (int64_t)bytes;
+    slot_chunk[slot] = -1;
+    return err == cudaSuccess ? cudaGetLastError() : err;
+  };
+
+  int64_t k = 0;
+  for (; k < nchunks; k++) {
+    const int slot = (int)(k % depth);
+    if (ex->cancel && ex->cancel(ex->cancel_ctx)) {
+      status = HB_ECANCELLED;
+      set_err(rep, "cancelled before chunk " + std::to_string(k));
+      break;
+    }
+    if (slot_chunk[slot] >= 0) {
+      e = finish(slot_chunk[slot]);
+      if (e != cudaSuccess) break;
+    }
+    if (ex->fault_chunk >= 0 && k == ex->fault_chunk) {
+      status = HB_ECHUNK;
+      set_err(rep, "injected fault on chunk " + std::to_string(k));
+      break;
+    }
+    const hb_chunk& c = chunks[k];
+    const int64_t ps = c.z_start - c.halo_lo;
+    const int64_t pn = c.z_stop + c.halo_hi - ps;
+    const int64_t n = c.z_stop - c.z_start;
+    const size_t in_bytes = (size_t)pn * plane * in_es;
+    const char* host_src = (const char*)in->data + (size_t)ps * plane * in_es;
+    // H2D (input buffer of this slot is free: its previous compute finished in finish())
+    if (in_pinned) {
+      e = cudaMemcpyAsync(dbuf_in[slot], host_src, in_bytes, cudaMemcpyHostToDevice, s_in);
+    } else {
+      e = h2d_staged(ring, dbuf_in[slot], host_src, in_bytes, s_in, threads);
+    }
+    if (e != cudaSuccess) break;
+    cudaEventRecord(ev_h2d[slot], s_in);
+    rep->h2d_bytes += (int64_t)in_bytes;
+    // compute
+    cudaStreamWaitEvent(s_comp, ev_h2d[slot], 0);
+    cudaEventRecord(ev_k0[slot], s_comp);
+    slots[slot].s = s_comp;
+    DevIn din{dbuf_in[slot], in->dtype, pn, in->ny, in->nx};
+    e = run_chain(st, din, c.halo_lo, n, dbuf_out[slot], slots[slot], s_comp, &launches);
+    slots[slot].release();
+    if (e != cudaSuccess) break;
+    cudaEventRecord(ev_comp[slot], s_comp);
+    // D2H straight into pinned output
+    if (out_pinned) {
+      cudaStreamWaitEvent(s_out, ev_comp[slot], 0);
+      char* host_dst = (char*)out->data + (size_t)c.z_start * plane * out_es;
+      e = cudaMemcpyAsync(host_dst, dbuf_out[slot], (size_t)n * plane * out_es,
+                          cudaMemcpyDeviceToHost, s_out);
+      if (e != cudaSuccess) break;
+      cudaEventRecord(ev_d2h[slot], s_out);
+      cudaEventRecord(ev_done[k], s_out);
+    }
+    slot_chunk[slot] = k;
+  }
+  // drain outstanding chunks in order
+  if (status == HB_OK && e == cudaSuccess) {
+    for (int64_t j = std::max<int64_t>(0, k - depth); j < k; j++) {
+      int slot = (int)(j % depth);
+      if (slot_chunk[slot] == j) {
+        e = finish(j);
+        if (e != cudaSuccess) break;
+      }
+    }
+  }
+  cudaError_t sync_e = cudaDeviceSynchronize();
+  if (e == cudaSuccess && status == HB_OK && sync_e != cudaSuccess) e = sync_e;
+  if (e != cudaSuccess && status == HB_OK) {
+    status = HB_ECUDA;
+    rep->failed_chunk = std::min<int64_t>(k, nchunks - 1);
+    set_err(rep, std::string("CUDA error on chunk ") + std::to_string(rep->failed_chunk) + ": " +
+                     cudaGetErrorString(e));
+    cudaGetLastError();
+  } else if (status != HB_OK) {
+    rep->failed_chunk = k;
+  }
+  if (status == HB_OK && ex->chunk_seconds) {
+    for (int64_t j = 0; j < nchunks; j++) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, j == 0 ? ev_start : ev_done[j - 1], ev_done[j]);
+      ex->chunk_seconds[j] = ms * 1e-3;
+    }
+  }
+  for (auto& sl : slots) sl.release();
+  io.release();
+  cudaStreamSynchronize(s_comp);
+  rep->device_peak_bytes = pool_attr(dev, cudaMemPoolAttrUsedMemHigh);
+  cudaMemPoolTrimTo(g_dev[dev].pool, 0);
+  rep->device_residual_bytes = pool_attr(dev, cudaMemPoolAttrReservedMemCurrent);
+  for (int i = 0; i < depth; i++) {
+    cudaEventDestroy(ev_h2d[i]);
+    cudaEventDestroy(ev_comp[i]);
+    cudaEventDestroy(ev_d2h[i]);
+    cudaEventDestroy(ev_k0[i]);
+  }
+  for (auto& v : ev_done) cudaEventDestroy(v);
+  cudaEventDestroy(ev_start);
+  cudaStreamDestroy(s_in);
+  cudaStreamDestroy(s_comp);
+  cudaStreamDestroy(s_out);
+  cudaGetLastError();
+  rep->chunk_count = nchunks;
+  rep->kernel_launches = launches;
+  rep->kernel_ms = kernel_ms;
+  rep->wall_ms = now_ms() - t_start;
+  return status;
+}
+
+}  // extern "C"

@@ -1,0 +1,79 @@
+// ops.cuh — internal launch API of the hot-path kernels (host side).
+//
+// Every kernel evaluates one map operator on a device block whose local z runs
+// over [0, in.nz) with clamp-to-edge at all six faces (exactly the padded-chunk
+// semantics of chunking.execute_chunked, chunking.py:248-257), and writes the
+// output slices [zo, zo + nzo) of that block.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace hb {
+
+constexpr int kMaxTaps = 129;  // R <= 64  (sigma <= 16)
+
+struct Taps {
+  float w[kMaxTaps];  // 2R+1 f32 weights (filters.py:26-30), w[R] is the centre
+  int R;
+};
+
+struct DevIn {
+  const void* p;
+  int dt;  // hb_dtype
+  int64_t nz, ny, nx;
+};
+
+// Epilogue of the last separable pass.
+enum Epi { EPI_NONE = 0, EPI_UNSHARP = 1, EPI_BOX_MEAN = 2 };
+
+struct EpiArgs {
+  int kind = EPI_NONE;
+  // unsharp: base = f32(orig[z + orig_zo]) (filters.py:136-139)
+  const void* orig = nullptr;
+  int orig_dt = HB_F32;
+  int64_t orig_zo = 0;
+  float amount = 0.f;
+  float inv_count = 1.f;  // box mean: divide by (2r+1)^3
+  float count = 1.f;
+};
+
+// --- separable stencils (sep.cu) ------------------------------------------
+// Gaussian (fast: fp32 FMA; exact: fp64 fold per pass, f32 round per pass,
+// axis order Z, Y, X as filters.py:38-40).  `tmp` must hold nzo*ny*nx floats.
+cudaError_t gaussian_generic(const DevIn& in, int64_t zo, int64_t nzo, float* out,
+                             const Taps& taps, bool exact, const EpiArgs& epi,
+                             float* tmp, cudaStream_t s, int64_t* launches);
+// Box mean of (2r+1)^3 (filters.py:66-75).
+cudaError_t mean_generic(const DevIn& in, int64_t zo, int64_t nzo, float* out, int r,
+                         float* tmp, cudaStream_t s, int64_t* launches);
+// LoG second stage: out = (cd_x cd_x g + cd_y cd_y g) + cd_z cd_z g, where the
+// smoothed block g covers local slices [gz0, gz0+ngz) of a block of `nz`
+// slices (clamps at [0, nz)) — filters.py:234-253.
+cudaError_t log_diff(const float* g, int64_t gz0, int64_t ngz, int64_t nz, int64_t ny,
+                     int64_t nx, int64_t zo, int64_t nzo, float* out, cudaStream_t s,
+                     int64_t* launches);
+// dtype conversion / copy (identity op, registry.py:127-133)
+cudaError_t copy_slices(const DevIn& in, int64_t zo, int64_t nzo, void* out,
+                        cudaStream_t s, int64_t* launches);
+
+// --- fused fast Gaussian family (gauss_fused.cu) --------------------------
+// Returns cudaErrorNotSupported when the shape/radius is outside the fused
+// kernel's envelope; the caller then uses the generic path.
+cudaError_t gaussian_fused(const DevIn& in, int64_t zo, int64_t nzo, float* out,
+                           const Taps& taps, const EpiArgs& epi, cudaStream_t s,
+                           int64_t* launches);
+
+// --- median (median.cu) ----------------------------------------------------
+cudaError_t median(const DevIn& in, int64_t zo, int64_t nzo, void* out, int r,
+                   cudaStream_t s, int64_t* launches);
+
+// --- flat grey morphology (morph.cu) --------------------------------------
+// offsets: 3*n ints (dz,dy,dx) host array; is_max selects dilation, in which
+// case the caller has already reflected the SE (morphology.py:119-121).
+cudaError_t morph(const DevIn& in, int64_t zo, int64_t nzo, void* out,
+                  const int32_t* offsets, int n, bool is_max, cudaStream_t s,
+                  int64_t* launches);
+
+}  // namespace hb

@@ -1,0 +1,131 @@
+"""Flat grey/binary morphology on the device (reference morphology.py:23-140).
+
+``StructuringElement`` keeps the reference's value semantics (offset tuples,
+``box``/``ball``/``cross``/``parse``/``reflect``/``extent``/``z_extent``) so
+registry params, CLI strings ("ball:3") and plans are interchangeable.  The
+window reduction itself (``_window_reduce``, morphology.py:103-111: edge pad
+then a min/max fold over every offset) runs in ``morph.cu``: the SE is
+decomposed into (dz, dy) rows of contiguous x-runs and each run's sliding
+min/max is computed once per slice.
+
+Binary morphology is the same code on {0, 1} uint8 volumes, exactly as in the
+reference (clamp-to-edge, not scipy's border_value=0).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native
+from .errors import ParameterError
+
+MORPH_OPS = ("erode", "dilate", "open", "close")
+
+
+def _check_radius(r):
+    if r < 1:
+        raise ParameterError(f"structuring element radius must be >= 1, got {r}")
+
+
+@dataclass(frozen=True)
+class StructuringElement:
+    """A set of integer (dz, dy, dx) displacements that contains the origin."""
+
+    offsets: tuple
+    name: str = "custom"
+
+    def __post_init__(self):
+        if not self.offsets:
+            raise ParameterError("structuring element must not be empty")
+        if (0, 0, 0) not in self.offsets:
+            raise ParameterError("structuring element must contain the origin")
+
+    @property
+    def extent(self) -> tuple:
+        arr = np.abs(np.asarray(self.offsets, dtype=np.int64))
+        return tuple(int(v) for v in arr.max(axis=0))
+
+    @property
+    def z_extent(self) -> int:
+        return self.extent[0]
+
+    def reflect(self) -> "StructuringElement":
+        return StructuringElement(tuple(sorted((-a, -b, -c) for a, b, c in self.offsets)),
+                                  name=self.name)
+
+    def as_array(self) -> np.ndarray:
+        return np.asarray(self.offsets, dtype=np.int32).reshape(-1, 3)
+
+    @staticmethod
+    def _cube(r):
+        rng = range(-r, r + 1)
+        return [(a, b, c) for a in rng for b in rng for c in rng]
+
+    @classmethod
+    def box(cls, r: int) -> "StructuringElement":
+        _check_radius(r)
+        return cls(tuple(cls._cube(r)), name=f"box:{r}")
+
+    @classmethod
+    def ball(cls, r: int) -> "StructuringElement":
+        # Euclidean norm in voxel units (morphology.py:60-71)
+        _check_radius(r)
+        return cls(tuple(o for o in cls._cube(r) if o[0] ** 2 + o[1] ** 2 + o[2] ** 2 <= r * r),
+                   name=f"ball:{r}")
+
+    @classmethod
+    def cross(cls, r: int) -> "StructuringElement":
+        _check_radius(r)
+        pts = {(0, 0, 0)}
+        for d in range(-r, r + 1):
+            pts.update({(d, 0, 0), (0, d, 0), (0, 0, d)})
+        return cls(tuple(sorted(pts)), name=f"cross:{r}")
+
+    @classmethod
+    def parse(cls, spec: str) -> "StructuringElement":
+        """'ball:2' / 'box:1' / 'cross:1' (morphology.py:84-95)."""
+        kind, _, r = str(spec).partition(":")
+        makers = {"box": cls.box, "ball": cls.ball, "cross": cls.cross}
+        if kind not in makers:
+            raise ParameterError(f"unknown structuring element {spec!r}")
+        try:
+            radius = int(r)
+        except ValueError:
+            raise ParameterError(f"bad structuring element radius in {spec!r}") from None
+        return makers[kind](radius)
+
+
+def morph_program(op: str, se: StructuringElement, iterations: int = 1) -> _native.DeviceProgram:
+    """Stage chain for morph(op, se, iterations) (morphology.py:124-140)."""
+    if op not in MORPH_OPS:
+        raise ParameterError(f"op must be one of {MORPH_OPS}, got {op!r}")
+    if iterations < 1:
+        raise ParameterError(f"iterations must be >= 1, got {iterations}")
+    off = se.as_array()
+    E = lambda: _native.Stage(_native.OP_ERODE, offsets=off)  # noqa: E731
+    D = lambda: _native.Stage(_native.OP_DILATE, offsets=off)  # noqa: E731 (library reflects)
+    one = {"erode": [E], "dilate": [D], "open": [E, D], "close": [D, E]}[op]
+    return _native.DeviceProgram([mk() for _ in range(iterations) for mk in one])
+
+
+def erode(data, se: StructuringElement):
+    """(I erode B)(p) = min_b I(p + b)."""
+    from .filters import apply_program
+
+    return apply_program(data, morph_program("erode", se))
+
+
+def dilate(data, se: StructuringElement):
+    """(I dilate B)(p) = max_b I(p - b)."""
+    from .filters import apply_program
+
+    return apply_program(data, morph_program("dilate", se))
+
+
+def morph(data, op: str, se: StructuringElement, iterations: int = 1):
+    """erode/dilate/open/close; open = dilate(erode(I)), close = erode(dilate(I))."""
+    from .filters import apply_program
+
+    return apply_program(data, morph_program(op, se, iterations))

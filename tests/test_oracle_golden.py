@@ -1,0 +1,67 @@
+"""The CPU oracle (oracle/) against fixtures generated from the reference.
+
+The oracle is the checker for every GPU parity test, so it is pinned here
+first: bit-exact against reference outputs for every case in tests/golden.
+"""
+import numpy as np
+import pytest
+
+
+def _run_case(O, case, arrays):
+    x = arrays[case["input"]]
+    op, p = case["op"], case["params"]
+    if op == "erode_offsets":
+        return O.erode(x, arrays[p["offsets"]])
+    if op == "dilate_offsets":
+        return O.dilate(x, arrays[p["offsets"]])
+    if op.startswith("morph_"):
+        return O.morph(x, op[6:], O.parse_se(p["se"]), p.get("iterations", 1))
+    return O.apply(op, x, p)
+
+
+def test_golden_cases_bit_exact(golden, oracle):
+    meta, arrays = golden
+    bad = []
+    for case in meta["cases"]:
+        got = _run_case(oracle, case, arrays)
+        want = arrays[case["output"]]
+        if got.dtype != want.dtype or not np.array_equal(got, want):
+            bad.append(case["name"])
+    assert not bad, f"oracle differs from the reference on {bad}"
+    assert len(meta["cases"]) >= 100
+
+
+def test_gaussian_weights_match_reference(golden, oracle):
+    meta, _ = golden
+    for sigma, w in meta["weights"].items():
+        np.testing.assert_array_equal(oracle.gaussian_weights(float(sigma)),
+                                      np.asarray(w, dtype=np.float32))
+
+
+def test_ball_sizes(golden, oracle):
+    meta, _ = golden
+    for r, n in meta["ball_sizes"].items():
+        assert len(oracle.ball_offsets(int(r))) == n
+    assert len(oracle.ball_offsets(3)) == 123
+
+
+def test_median_brute_force(oracle, rng):
+    # reference test_filters.py:82-86 — independent sort oracle
+    data = rng.integers(0, 256, size=(5, 6, 7), dtype=np.uint8)
+    got = oracle.median(data, 1)
+    pad = np.pad(data, 1, mode="edge")
+    for i in range(5):
+        for j in range(6):
+            for k in range(7):
+                assert got[i, j, k] == np.sort(pad[i:i + 3, j:j + 3, k:k + 3].ravel())[13]
+
+
+def test_gaussian_impulse_is_separable_kernel(oracle):
+    # reference test_filters.py:27-39
+    data = np.zeros((17, 17, 17), np.float32)
+    data[8, 8, 8] = 1
+    out = oracle.gaussian(data, 1.0)
+    k = oracle.gaussian_weights(1.0).astype(np.float64)
+    r = (k.size - 1) // 2
+    exp = k[:, None, None] * k[None, :, None] * k[None, None, :]
+    assert np.max(np.abs(out[8 - r:9 + r, 8 - r:9 + r, 8 - r:9 + r] - exp)) <= 1e-6
