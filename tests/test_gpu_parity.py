@@ -233,7 +233,7 @@ def test_pipeline_matches_sequential(hb):
     steps = [("unsharp", {"sigma": 1.0, "amount": 1.5}), ("log", {"sigma": 2.0})]
     seq = registry.run_direct(registry.run_direct(x, *steps[0]), *steps[1])
     from paper_2511_11890_b200.chunking import MemoryBudget
-    got, rep = registry.run_pipeline(x, steps, MemoryBudget(20 * 40 * 36 * 4 * 10, 1.0))
+    got, rep = registry.run_pipeline(x, steps, MemoryBudget(40 * 40 * 36 * 4 * 10, 1.0))
     assert rep.chunk_count > 1
     assert np.array_equal(got, seq)
 
