@@ -65,6 +65,9 @@ cudaError_t gaussian_fused(const DevIn& in, int64_t zo, int64_t nzo, float* out,
                            const Taps& taps, const EpiArgs& epi, cudaStream_t s,
                            int64_t* launches);
 
+cudaError_t mean_fused(const DevIn& in, int64_t zo, int64_t nzo, float* out, int r,
+                       cudaStream_t s, int64_t* launches);
+
 // --- median (median.cu) ----------------------------------------------------
 cudaError_t median(const DevIn& in, int64_t zo, int64_t nzo, void* out, int r,
                    cudaStream_t s, int64_t* launches);
