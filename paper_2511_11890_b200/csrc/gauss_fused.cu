@@ -276,8 +276,9 @@ k_sep3d_fused(const __grid_constant__ CUtensorMap tin, const __grid_constant__ C
                 fmaf(ring[(U + 1 + R - d) % G::RING][m] + ring[(U + 1 + R + d) % G::RING][m], \
                      w[R - d], acc);                                              \
           } else {                                                                \
-            acc = ring[0][m];                                                     \
-            _Pragma("unroll") for (int k = 1; k < G::RING; ++k) acc += ring[k][m]; \
+            acc = ring[(U + 1) % G::RING][m];                                     \
+            _Pragma("unroll") for (int k = 1; k < G::RING; ++k) acc +=            \
+                ring[(U + 1 + k) % G::RING][m]; /* z order: plan invariant */     \
           }                                                                       \
           zo_[m] = acc;                                                           \
         }                                                                         \

@@ -2,10 +2,14 @@
 // (filters.py:78-82 -> scipy median_filter -> rank_filter).  Output dtype is
 // the input dtype; the order statistic is exact, so results are bit-exact.
 //
-// r = 1, 2: forgetful selection in registers (working set N/2+2, each round
-// discards the min and max of the set and admits one new sample).
+// r = 1:    plane formulation with shared sorted planes (k_median3_plane).
+// r = 2:    forgetful selection in registers (working set N/2+2, each round
+//           discards the min and max of the set and admits one new sample).
 // r >= 3:   per-voxel radix (bit-by-bit) selection over order-preserving keys.
+#include <algorithm>
+
 #include "ops.cuh"
+#include "median_nets.h"
 
 namespace hb {
 namespace {
@@ -151,6 +155,207 @@ k_median_radix(const T* __restrict__ in, int64_t nz, int64_t ny, int64_t nx, int
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// 3x3x3 median, plane formulation (the fast path for r = 1)
+//
+// Output (z, y, x) = rank 13 of P(z-1) ∪ P(z) ∪ P(z+1), where P(s) is the sorted
+// 3x3 XY neighbourhood of slice s.  Each thread owns two adjacent x columns and
+// marches down z, so every plane is sorted once and used by three outputs:
+//   plane sort : rows sort3 -> columns sort3 (3x3 Young tableau) -> 7 comparators
+//   merge      : P(z) ∪ P(z+1) pruned to ranks 4..13 (27 comparators, generated)
+//   select     : rank13 = min_{i+j=14} max(M[i-1], P(z-1)[j-1])
+// All comparisons run on order-preserving int32 keys so that half of every
+// compare-exchange runs on the FMA pipe: max(a,b) = (a + b) - min(a,b) (exact
+// mod 2^32) via IMAD with a runtime multiplier ptxas cannot fold.
+// ---------------------------------------------------------------------------
+struct ImadOnes {
+  int one, mone;  // runtime 1 and -1 (kernel params) -> IMAD, not IADD3
+};
+
+__device__ __forceinline__ int imad(int a, int b, int c) {
+  int d;
+  asm("mad.lo.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
+template <typename T> __device__ __forceinline__ int to_key(T v) { return (int)v; }
+template <> __device__ __forceinline__ int to_key<uint32_t>(uint32_t v) { return (int)(v ^ 0x80000000u); }
+template <> __device__ __forceinline__ int to_key<float>(float v) {
+  const int u = __float_as_int(v);
+  return u ^ ((u >> 31) & 0x7fffffff);
+}
+template <typename T> __device__ __forceinline__ T from_key(int k) { return (T)k; }
+template <> __device__ __forceinline__ uint32_t from_key<uint32_t>(int k) { return (uint32_t)k ^ 0x80000000u; }
+template <> __device__ __forceinline__ float from_key<float>(int k) {
+  return __int_as_float(k ^ ((k >> 31) & 0x7fffffff));
+}
+
+struct Net {
+  ImadOnes c;
+  // compare-exchange: a <- min, b <- max (max from the sum on the FMA pipe)
+  __device__ __forceinline__ void ce(int& a, int& b) const {
+    const int lo = min(a, b);
+    const int s = imad(a, c.one, b);
+    b = imad(lo, c.mone, s);
+    a = lo;
+  }
+  __device__ __forceinline__ void sort3(int& a, int& b, int& cc) const {
+    const int lo = min(a, min(b, cc));
+    const int hi = max(a, max(b, cc));
+    int t = imad(a, c.one, b);
+    t = imad(cc, c.one, t);
+    t = imad(lo, c.mone, t);
+    b = imad(hi, c.mone, t);
+    a = lo;
+    cc = hi;
+  }
+  // sorted 3x3 neighbourhood: in r[row][col] (row-major), out s[0..8] ascending
+  __device__ __forceinline__ void plane(int (&r)[3][3], int (&s)[9]) const {
+#pragma unroll
+    for (int i = 0; i < 3; ++i) sort3(r[i][0], r[i][1], r[i][2]);  // rows
+#pragma unroll
+    for (int j = 0; j < 3; ++j) sort3(r[0][j], r[1][j], r[2][j]);  // columns
+    // tableau -> sorted, wire order (0,0),(0,1),(1,0),(0,2),(1,1),(2,0),(1,2),(2,1),(2,2)
+    s[0] = r[0][0]; s[1] = r[0][1]; s[2] = r[1][0]; s[3] = r[0][2]; s[4] = r[1][1];
+    s[5] = r[2][0]; s[6] = r[1][2]; s[7] = r[2][1]; s[8] = r[2][2];
+    ce(s[3], s[5]); ce(s[1], s[2]); ce(s[2], s[3]); ce(s[6], s[7]);
+    ce(s[5], s[6]); ce(s[3], s[4]); ce(s[4], s[5]);
+  }
+  // rank 13 of prev ∪ cur ∪ nxt (all sorted 9-lists)
+  __device__ __forceinline__ int med27(const int (&prev)[9], const int (&cur)[9],
+                                       const int (&nxt)[9]) const {
+    int w[18];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) {
+      w[i] = cur[i];
+      w[9 + i] = nxt[i];
+    }
+#define HB_CE(i, j) ce(w[i], w[j]);
+#define HB_MN(i, j) w[i] = min(w[i], w[j]);
+#define HB_MX(i, j) w[j] = max(w[i], w[j]);
+    HB_MERGE9_RANK4_13(HB_CE, HB_MN, HB_MX)
+#undef HB_CE
+#undef HB_MN
+#undef HB_MX
+    // select: min over j=0..9 of max(M[13-j], prev[j-1]); M[r] = w[r]
+    int t0 = w[13];
+    int t1 = max(w[12], prev[0]);
+    int t2 = max(w[11], prev[1]);
+    int t3 = max(w[10], prev[2]);
+    int t4 = max(w[9], prev[3]);
+    int t5 = max(w[8], prev[4]);
+    int t6 = max(w[7], prev[5]);
+    int t7 = max(w[6], prev[6]);
+    int t8 = max(w[5], prev[7]);
+    int t9 = max(w[4], prev[8]);
+    return min(min(min(t0, t1), min(t2, t3)), min(min(min(t4, t5), min(t6, t7)), min(t8, t9)));
+  }
+};
+
+constexpr int M3_TX = 64, M3_TY = 8;  // outputs per CTA slice (32 x-pairs x 8 rows)
+constexpr int M3_W = M3_TX + 2, M3_H = M3_TY + 2;
+
+template <typename T>
+__global__ void __launch_bounds__(256, 2)
+k_median3_plane(const T* __restrict__ in, int64_t nz, int64_t ny, int64_t nx, int64_t zo,
+                int64_t nzo, int zchunk, T* __restrict__ out, ImadOnes ones) {
+  __shared__ __align__(16) int tile[2][M3_H][M3_W];
+  const Net net{ones};
+  const int tid = threadIdx.x;
+  const int tx = tid & 31, ty = tid >> 5;
+  const int64_t x0 = (int64_t)blockIdx.x * M3_TX, y0 = (int64_t)blockIdx.y * M3_TY;
+  const int64_t zs = (int64_t)blockIdx.z * zchunk;
+  const int64_t ze = min(zs + (int64_t)zchunk, nzo);
+  // cooperative slice loader: element e of the halo'd tile -> (ly, lx)
+  constexpr int NE = M3_H * M3_W;
+  constexpr int PER = (NE + 255) / 256;
+  int64_t goff[PER];
+  bool gval[PER];
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const int e = tid + 256 * k;
+    gval[k] = e < NE;
+    const int ly = gval[k] ? e / M3_W : 0, lx = gval[k] ? e % M3_W : 0;
+    const int64_t gy = clamp64(y0 - 1 + ly, 0, ny - 1), gx = clamp64(x0 - 1 + lx, 0, nx - 1);
+    goff[k] = gy * nx + gx;
+  }
+  auto fetch = [&](int64_t zb, int (&v)[PER]) {
+    const T* src = in + clamp64(zb, 0, nz - 1) * ny * nx;
+#pragma unroll
+    for (int k = 0; k < PER; ++k) v[k] = gval[k] ? to_key<T>(__ldg(src + goff[k])) : 0;
+  };
+  auto stash = [&](int buf, const int (&v)[PER]) {
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int e = tid + 256 * k;
+      if (gval[k]) (&tile[buf][0][0])[e] = v[k];
+    }
+  };
+  // this thread's two planes of slice `buf`
+  auto planes = [&](int buf, int (&pa)[9], int (&pb)[9]) {
+    int r[3][4];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const int2 lo = *reinterpret_cast<const int2*>(&tile[buf][ty + i][2 * tx]);
+      const int2 hi = *reinterpret_cast<const int2*>(&tile[buf][ty + i][2 * tx + 2]);
+      r[i][0] = lo.x; r[i][1] = lo.y; r[i][2] = hi.x; r[i][3] = hi.y;
+    }
+    int a[3][3], b[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        a[i][j] = r[i][j];
+        b[i][j] = r[i][j + 1];
+      }
+    net.plane(a, pa);
+    net.plane(b, pb);
+  };
+  const int64_t gy = y0 + ty, gx = x0 + 2 * tx;
+  const bool st_y = gy < ny, st_x0 = gx < nx, st_x1 = gx + 1 < nx;
+  T* orow = out + gy * nx + gx;
+  auto emit = [&](int64_t z, int k0, int k1) {
+    if (!st_y) return;
+    T* o = orow + (z - zo) * ny * nx;
+    if (st_x0) o[0] = from_key<T>(k0);
+    if (st_x1) o[1] = from_key<T>(k1);
+  };
+
+  // block z of output slice z (output-local) is zo + z; planes indexed by block z
+  int P[3][2][9];
+  int v[PER];
+  fetch(zo + zs - 1, v);
+  stash(0, v);
+  fetch(zo + zs, v);
+  __syncthreads();
+  planes(0, P[0][0], P[0][1]);  // slice zs-1
+  stash(1, v);
+  fetch(zo + zs + 1, v);
+  __syncthreads();
+  planes(1, P[1][0], P[1][1]);  // slice zs
+  // rotating buffers: tile buffer of slice (zs + k) is (k + 1) & 1
+  int64_t z = zs;
+  while (z < ze) {
+#pragma unroll
+    for (int u = 0; u < 3; ++u) {
+      if (z < ze) {
+        const int pb = (u + 2) % 3, pp = u % 3, pc = (u + 1) % 3;  // next, prev, cur
+        const int tb = (int)((z - zs) & 1);  // buffer for slice z+1
+        __syncthreads();                     // everyone done reading tb (slice z-1)
+        stash(tb, v);
+        fetch(zo + z + 2, v);
+        __syncthreads();
+        planes(tb, P[pb][0], P[pb][1]);
+        const int m0 = net.med27(P[pp][0], P[pc][0], P[pb][0]);
+        const int m1 = net.med27(P[pp][1], P[pc][1], P[pb][1]);
+        emit(zo + z, m0, m1);
+        ++z;
+      }
+    }
+  }
+}
+
 inline int grid_for(int64_t n) {
   int64_t b = (n + kThreads - 1) / kThreads;
   int64_t cap = (int64_t)kNumSMs * 16;
@@ -165,7 +370,13 @@ cudaError_t run_median(const DevIn& in, int64_t zo, int64_t nzo, void* out, int 
   const T* src = (const T*)in.p;
   T* dst = (T*)out;
   if (r == 1) {
-    k_median_forgetful<1, T, K><<<g, kThreads, 0, s>>>(src, in.nz, in.ny, in.nx, zo, nzo, dst);
+    dim3 grid((unsigned)((in.nx + M3_TX - 1) / M3_TX), (unsigned)((in.ny + M3_TY - 1) / M3_TY), 1);
+    const int64_t tiles = (int64_t)grid.x * grid.y;
+    const int64_t want = std::max<int64_t>(1, (8 * kNumSMs + tiles - 1) / tiles);
+    const int zchunk = (int)std::max<int64_t>(16, (nzo + want - 1) / want);
+    grid.z = (unsigned)((nzo + zchunk - 1) / zchunk);
+    k_median3_plane<T><<<grid, 256, 0, s>>>(src, in.nz, in.ny, in.nx, zo, nzo, zchunk, dst,
+                                            ImadOnes{1, -1});
   } else if (r == 2) {
     k_median_forgetful<2, T, K><<<g, kThreads, 0, s>>>(src, in.nz, in.ny, in.nx, zo, nzo, dst);
   } else {
