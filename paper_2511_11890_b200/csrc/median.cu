@@ -222,9 +222,8 @@ struct Net {
     ce(s[3], s[5]); ce(s[1], s[2]); ce(s[2], s[3]); ce(s[6], s[7]);
     ce(s[5], s[6]); ce(s[3], s[4]); ce(s[4], s[5]);
   }
-  // rank 13 of prev ∪ cur ∪ nxt (all sorted 9-lists)
-  __device__ __forceinline__ int med27(const int (&prev)[9], const int (&cur)[9],
-                                       const int (&nxt)[9]) const {
+  // ranks 4..13 of cur ∪ nxt (two sorted 9-lists) -> m[0..9]
+  __device__ __forceinline__ void merge(const int (&cur)[9], const int (&nxt)[9], int (&m)[10]) const {
     int w[18];
 #pragma unroll
     for (int i = 0; i < 9; ++i) {
@@ -238,17 +237,22 @@ struct Net {
 #undef HB_CE
 #undef HB_MN
 #undef HB_MX
-    // select: min over j=0..9 of max(M[13-j], prev[j-1]); M[r] = w[r]
-    int t0 = w[13];
-    int t1 = max(w[12], prev[0]);
-    int t2 = max(w[11], prev[1]);
-    int t3 = max(w[10], prev[2]);
-    int t4 = max(w[9], prev[3]);
-    int t5 = max(w[8], prev[4]);
-    int t6 = max(w[7], prev[5]);
-    int t7 = max(w[6], prev[6]);
-    int t8 = max(w[5], prev[7]);
-    int t9 = max(w[4], prev[8]);
+#pragma unroll
+    for (int i = 0; i < 10; ++i) m[i] = w[4 + i];
+  }
+  // rank 13 of M ∪ P where M holds ranks 4..13 of two planes and P is the
+  // third sorted plane: min over j=0..9 of max(M[13-j], P[j-1])
+  __device__ __forceinline__ int select(const int (&m)[10], const int (&p)[9]) const {
+    const int t0 = m[9];
+    const int t1 = max(m[8], p[0]);
+    const int t2 = max(m[7], p[1]);
+    const int t3 = max(m[6], p[2]);
+    const int t4 = max(m[5], p[3]);
+    const int t5 = max(m[4], p[4]);
+    const int t6 = max(m[3], p[5]);
+    const int t7 = max(m[2], p[6]);
+    const int t8 = max(m[1], p[7]);
+    const int t9 = max(m[0], p[8]);
     return min(min(min(t0, t1), min(t2, t3)), min(min(min(t4, t5), min(t6, t7)), min(t8, t9)));
   }
 };
@@ -322,37 +326,52 @@ k_median3_plane(const T* __restrict__ in, int64_t nz, int64_t ny, int64_t nx, in
     if (st_x1) o[1] = from_key<T>(k1);
   };
 
-  // block z of output slice z (output-local) is zo + z; planes indexed by block z
-  int P[3][2][9];
+  // One merge serves two outputs: out(z) = sel(M, P(z-1)), out(z+1) = sel(M, P(z+2))
+  // with M = ranks 4..13 of P(z) ∪ P(z+1).  Four steps cycle the plane names.
+  int X[2][9], Y[2][9], Z[2][9], W[2][9], M[2][10];
   int v[PER];
   fetch(zo + zs - 1, v);
   stash(0, v);
   fetch(zo + zs, v);
   __syncthreads();
-  planes(0, P[0][0], P[0][1]);  // slice zs-1
+  planes(0, X[0], X[1]);  // P(zs-1)
   stash(1, v);
   fetch(zo + zs + 1, v);
   __syncthreads();
-  planes(1, P[1][0], P[1][1]);  // slice zs
-  // rotating buffers: tile buffer of slice (zs + k) is (k + 1) & 1
+  planes(1, Y[0], Y[1]);  // P(zs)
   int64_t z = zs;
+  int tb = 0;  // smem buffer that receives slice z+1
+  auto next_plane = [&](int (&pa)[9], int (&pb)[9]) {
+    __syncthreads();  // everyone finished reading buffer tb (slice z-1)
+    stash(tb, v);
+    fetch(zo + z + 2, v);
+    __syncthreads();
+    planes(tb, pa, pb);
+    tb ^= 1;
+  };
+  auto emit2 = [&](int m0, int m1) {
+    emit(zo + z, m0, m1);
+    ++z;
+  };
   while (z < ze) {
-#pragma unroll
-    for (int u = 0; u < 3; ++u) {
-      if (z < ze) {
-        const int pb = (u + 2) % 3, pp = u % 3, pc = (u + 1) % 3;  // next, prev, cur
-        const int tb = (int)((z - zs) & 1);  // buffer for slice z+1
-        __syncthreads();                     // everyone done reading tb (slice z-1)
-        stash(tb, v);
-        fetch(zo + z + 2, v);
-        __syncthreads();
-        planes(tb, P[pb][0], P[pb][1]);
-        const int m0 = net.med27(P[pp][0], P[pc][0], P[pb][0]);
-        const int m1 = net.med27(P[pp][1], P[pc][1], P[pb][1]);
-        emit(zo + z, m0, m1);
-        ++z;
-      }
-    }
+    // state: X = P(z-1), Y = P(z)
+    next_plane(Z[0], Z[1]);  // P(z+1)
+    net.merge(Y[0], Z[0], M[0]);
+    net.merge(Y[1], Z[1], M[1]);
+    emit2(net.select(M[0], X[0]), net.select(M[1], X[1]));
+    if (z >= ze) break;
+    next_plane(W[0], W[1]);  // P(z+2)  (z already advanced)
+    emit2(net.select(M[0], W[0]), net.select(M[1], W[1]));
+    if (z >= ze) break;
+    // state: Z = P(z-1), W = P(z)
+    next_plane(X[0], X[1]);
+    net.merge(W[0], X[0], M[0]);
+    net.merge(W[1], X[1], M[1]);
+    emit2(net.select(M[0], Z[0]), net.select(M[1], Z[1]));
+    if (z >= ze) break;
+    next_plane(Y[0], Y[1]);
+    emit2(net.select(M[0], Y[0]), net.select(M[1], Y[1]));
+    // state: X = P(z-1), Y = P(z)
   }
 }
 
