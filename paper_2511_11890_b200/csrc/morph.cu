@@ -13,6 +13,7 @@
 #include <map>
 
 #include "ops.cuh"
+#include "tma.cuh"
 
 namespace hb {
 namespace {
@@ -181,11 +182,327 @@ cudaError_t run_morph(const DevIn& in, int64_t zo, int64_t nzo, void* out, const
   return cudaGetLastError();
 }
 
+
+// ===========================================================================
+// v2: TMA-fed, shape-shared erosion/dilation for u8/u16 with odd centred runs
+// ---------------------------------------------------------------------------
+// The SE's dz-layers are 2D shapes; identical shapes (e.g. +dz and -dz of a
+// ball) are evaluated once per slice.  Per input slice:
+//   H: every halo'd row computes run-min/max of each needed odd length L
+//      (run_{L+2}(c) = op(run_L(c+1), raw[c], raw[c+L+1]) -> one 3-input op per
+//      length) and stores packed u16x2 pairs (run(c), run(c+1)) in smem;
+//   V: each thread folds the rows of every distinct shape for its output pair
+//      with min/max.u16x2 (two voxels per instruction);
+//   Z: the shape values are pushed into a (2*EZ+1)-deep register ring of
+//      pending outputs; the oldest output is complete and stored.
+// ===========================================================================
+constexpr int M2_TX = 64, M2_TY = 16, M2_NT = 256, M2_NST = 3;
+constexpr int M2_MAXL = 8, M2_MAXSH = 9, M2_MAXROWS = 96;
+
+struct Morph2Args {
+  int nzi, zo, nzo, zchunk, nx, ny;
+  int ez, ey, ex;
+  int xa, wbox, hy, wc;          // smem geometry of the raw stage
+  int n_lens;
+  int lens[M2_MAXL];             // ascending odd run lengths (1 = raw)
+  int n_shapes;
+  int shape_of_dz[17];           // dz + ez -> shape id
+  int row_begin[M2_MAXSH + 1];   // rows of shape k: [row_begin[k], row_begin[k+1])
+  int row_off[M2_MAXROWS];       // (dy + ey) * wc + ex + lo  (index into a run array)
+  int row_len[M2_MAXROWS];       // index into lens
+  int off_runs, stage_pitch, off_bar;
+};
+
+template <bool MAX>
+__device__ __forceinline__ uint32_t op2x2(uint32_t a, uint32_t b) {
+  uint32_t d;
+  if (MAX) asm("max.u16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  else asm("min.u16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+template <bool MAX>
+__device__ __forceinline__ uint32_t op1(uint32_t a, uint32_t b) { return MAX ? max(a, b) : min(a, b); }
+
+template <typename T, bool MAX, int EZ>
+__global__ void __launch_bounds__(M2_NT, 2)
+k_morph2(const __grid_constant__ CUtensorMap tin, T* __restrict__ out, const Morph2Args a) {
+  constexpr int RING = 2 * EZ + 1;
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem =
+      reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~(uintptr_t)127);
+  T* sraw = reinterpret_cast<T*>(smem);
+  uint32_t* runs = reinterpret_cast<uint32_t*>(smem + a.off_runs);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + a.off_bar);
+  const int tid = threadIdx.x;
+  const int x0 = blockIdx.x * M2_TX, y0 = blockIdx.y * M2_TY;
+  const int z0 = blockIdx.z * a.zchunk;
+  const int z1 = min(z0 + a.zchunk, a.nzo);
+  const int nsl = (z1 - z0) + 2 * EZ;
+  const bool border = (x0 - a.ex < 0) || (x0 + M2_TX + a.ex > a.nx) || (y0 - a.ey < 0) ||
+                      (y0 + M2_TY + a.ey > a.ny);
+  const int xoff = a.xa - a.ex;
+  const int stage_elems = a.stage_pitch / (int)sizeof(T);
+  const uint32_t box_bytes = (uint32_t)(a.hy * a.wbox * sizeof(T));
+  const int run_plane = a.hy * a.wc;  // uint32 entries per run length
+  auto zin_of = [&](int s) { return min(max(a.zo + z0 - EZ + s, 0), a.nzi - 1); };
+
+  if (tid == 0) {
+    prefetch_tmap(&tin);
+    for (int i = 0; i < M2_NST; ++i) mbar_init(&bar[i], 1);
+    fence_mbar_init();
+    for (int i = 0; i < M2_NST && i < nsl; ++i) {
+      mbar_expect_tx(&bar[i], box_bytes);
+      tma_load_3d(sraw + i * stage_elems, &tin, x0 - a.xa, y0 - a.ey, zin_of(i), &bar[i]);
+    }
+  }
+  __syncthreads();
+
+  const int px = tid & 31, ty = tid >> 5;  // output pair px (x = 2px), rows ty, ty+8
+  uint32_t acc[2][RING];
+#pragma unroll
+  for (int r = 0; r < 2; ++r)
+#pragma unroll
+    for (int u = 0; u < RING; ++u) acc[r][u] = MAX ? 0u : 0xffffffffu;
+  const int lmax = a.lens[a.n_lens - 1];
+  const int nseg = (a.wc + 7) / 8;
+
+  for (int s = 0; s < nsl; ++s) {
+    const int st = s % M2_NST;
+    T* stage = sraw + st * stage_elems;
+    mbar_wait(&bar[st], (uint32_t)((s / M2_NST) & 1));
+    if (border) {
+      for (int e = tid; e < a.hy * a.wc; e += M2_NT) {
+        const int ly = e / a.wc, lx = e - ly * a.wc;
+        const int gy = y0 - a.ey + ly, gx = x0 - a.ex + lx;
+        const int cy = min(max(gy, 0), a.ny - 1), cx = min(max(gx, 0), a.nx - 1);
+        if (cy != gy || cx != gx)
+          stage[ly * a.wbox + xoff + lx] = stage[(cy - (y0 - a.ey)) * a.wbox + xoff + (cx - (x0 - a.ex))];
+      }
+      fence_proxy_async();
+      __syncthreads();
+    }
+    // ---- H: runs of every length for 8 consecutive columns per item -------
+    for (int item = tid; item < a.hy * nseg; item += M2_NT) {
+      const int r = item / nseg, c0 = (item - r * nseg) * 8;
+      const T* row = stage + r * a.wbox + xoff;
+      uint32_t raw[8 + 2 * 8 + 2];  // c0 .. c0 + 9 + lmax (clamped to the row)
+      const int need = 9 + lmax;
+#pragma unroll
+      for (int i = 0; i < 26; ++i)
+        if (i < need) raw[i] = (uint32_t)row[min(c0 + i, a.wc - 1)];
+      // run_L(c0 + i) for i = 0..17; position i at step t needs i+1 at step t-1,
+      // so 18 entries keep i <= 8 exact for up to 8 steps (L <= 17)
+      uint32_t run[18];
+#pragma unroll
+      for (int i = 0; i < 18; ++i) run[i] = raw[i];
+      int li = 0;
+#pragma unroll
+      for (int step = 0; step <= 8; ++step) {
+        const int L = 2 * step + 1;
+        if (li < a.n_lens && a.lens[li] == L) {
+          uint32_t* dst = runs + li * run_plane + r * a.wc + c0;
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            if (c0 + i < a.wc) dst[i] = run[i] | (run[i + 1] << 16);
+          ++li;
+        }
+        if (L >= lmax) break;
+        // run_{L+2}(c) = op(run_L(c+1), raw[c], raw[c+L+1])
+#pragma unroll
+        for (int i = 0; i < 18; ++i) {
+          const uint32_t inner = run[i < 17 ? i + 1 : 17];
+          run[i] = op1<MAX>(op1<MAX>(inner, raw[i]), raw[(i + L + 1) < 26 ? (i + L + 1) : 25]);
+        }
+      }
+    }
+    __syncthreads();
+    if (tid == 0 && s + M2_NST < nsl) {
+      fence_proxy_async();
+      mbar_expect_tx(&bar[st], box_bytes);
+      tma_load_3d(stage, &tin, x0 - a.xa, y0 - a.ey, zin_of(s + M2_NST), &bar[st]);
+    }
+    // ---- V + Z --------------------------------------------------------------
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr) {
+      const int yo = ty + 8 * rr;
+      const int base = yo * a.wc + 2 * px;
+      uint32_t shape_val[M2_MAXSH];
+#pragma unroll
+      for (int k = 0; k < M2_MAXSH; ++k) {
+        if (k < a.n_shapes) {
+          uint32_t v = MAX ? 0u : 0xffffffffu;
+          for (int q = a.row_begin[k]; q < a.row_begin[k + 1]; ++q)
+            v = op2x2<MAX>(v, runs[a.row_len[q] * run_plane + base + a.row_off[q]]);
+          shape_val[k] = v;
+        }
+      }
+      // slice s sits at dz = s - z from pending output z (z = s - EZ .. s + EZ)
+      switch (s % RING) {
+#define HB_M2_CASE(U)                                                              \
+  case U:                                                                          \
+    if constexpr (U < RING) {                                                      \
+      _Pragma("unroll") for (int d = -EZ; d <= EZ; ++d) {                          \
+        /* output z = s - d lives in ring slot (U - d) mod RING */                 \
+        const int sh = a.shape_of_dz[d + EZ];                                      \
+        uint32_t sv = shape_val[0];                                                \
+        _Pragma("unroll") for (int k = 1; k < M2_MAXSH; ++k) if (k == sh) sv = shape_val[k]; \
+        if (sh >= 0) acc[rr][((U - d) % RING + RING) % RING] =                     \
+            op2x2<MAX>(acc[rr][((U - d) % RING + RING) % RING], sv);               \
+      }                                                                            \
+      {                                                                            \
+        const int o = s - 2 * EZ; /* output (chunk-local) completed now */        \
+        const int slot = ((U - EZ) % RING + RING) % RING;                          \
+        if (o >= 0) {                                                              \
+          const int gy = y0 + yo, gx = x0 + 2 * px;                                \
+          if (gy < a.ny && gx < a.nx) {                                            \
+            T* dst = out + ((int64_t)(z0 + o) * a.ny + gy) * (int64_t)a.nx + gx;    \
+            const uint32_t v = acc[rr][slot];                                      \
+            dst[0] = (T)(v & 0xffffu);                                             \
+            if (gx + 1 < a.nx) dst[1] = (T)(v >> 16);                              \
+          }                                                                        \
+        }                                                                          \
+        acc[rr][slot] = MAX ? 0u : 0xffffffffu;                                    \
+      }                                                                            \
+    }                                                                              \
+    break;
+        HB_M2_CASE(0) HB_M2_CASE(1) HB_M2_CASE(2) HB_M2_CASE(3) HB_M2_CASE(4)
+        HB_M2_CASE(5) HB_M2_CASE(6) HB_M2_CASE(7) HB_M2_CASE(8)
+#undef HB_M2_CASE
+        default: break;
+      }
+    }
+    __syncthreads();  // runs are rewritten by the next slice's H phase
+  }
+}
+
+// host-side builder for Morph2Args; false if the SE is outside v2's envelope
+bool build_morph2(const int32_t* off, int n, Morph2Args& a) {
+  std::map<int, std::map<int, std::vector<int>>> layers;  // dz -> dy -> dx list
+  int ez = 0, ey = 0, ex = 0;
+  for (int k = 0; k < n; ++k) {
+    const int dz = off[3 * k], dy = off[3 * k + 1], dx = off[3 * k + 2];
+    layers[dz][dy].push_back(dx);
+    ez = std::max(ez, std::abs(dz));
+    ey = std::max(ey, std::abs(dy));
+    ex = std::max(ex, std::abs(dx));
+  }
+  if (ez > 4 || ey > 8 || ex > 8) return false;
+  a.ez = ez; a.ey = ey; a.ex = ex;
+  // rows: each (dz, dy) must be one contiguous dx run of odd length centred at 0
+  std::vector<std::vector<std::pair<int, int>>> shapes;  // list of (dy, len)
+  for (int i = 0; i < 17; ++i) a.shape_of_dz[i] = -1;
+  std::vector<int> lens;
+  for (auto& L : layers) {
+    std::vector<std::pair<int, int>> rows;
+    for (auto& R : L.second) {
+      std::vector<int> v = R.second;
+      std::sort(v.begin(), v.end());
+      v.erase(std::unique(v.begin(), v.end()), v.end());
+      const int lo = v.front(), hi = v.back();
+      if ((int)v.size() != hi - lo + 1 || lo != -hi) return false;  // contiguous, centred
+      rows.push_back({R.first, hi - lo + 1});
+      lens.push_back(hi - lo + 1);
+    }
+    int id = -1;
+    for (size_t k = 0; k < shapes.size(); ++k)
+      if (shapes[k] == rows) id = (int)k;
+    if (id < 0) {
+      id = (int)shapes.size();
+      shapes.push_back(rows);
+    }
+    a.shape_of_dz[L.first + ez] = id;
+  }
+  std::sort(lens.begin(), lens.end());
+  lens.erase(std::unique(lens.begin(), lens.end()), lens.end());
+  if ((int)lens.size() > M2_MAXL || (int)shapes.size() > M2_MAXSH) return false;
+  a.n_lens = (int)lens.size();
+  for (int i = 0; i < a.n_lens; ++i) a.lens[i] = lens[i];
+  a.n_shapes = (int)shapes.size();
+  a.wc = M2_TX + 2 * ex;
+  int q = 0;
+  for (int k = 0; k < a.n_shapes; ++k) {
+    a.row_begin[k] = q;
+    for (auto& rl : shapes[k]) {
+      if (q >= M2_MAXROWS) return false;
+      const int li = (int)(std::find(lens.begin(), lens.end(), rl.second) - lens.begin());
+      const int half = (rl.second - 1) / 2;
+      a.row_off[q] = (rl.first + ey) * a.wc + ex - half;
+      a.row_len[q] = li;
+      ++q;
+    }
+  }
+  a.row_begin[a.n_shapes] = q;
+  return true;
+}
+
+template <typename T, bool MAX, int EZ>
+cudaError_t launch_morph2(const DevIn& in, int64_t zo, int64_t nzo, void* out, Morph2Args a,
+                          cudaStream_t s) {
+  const int align = 16 / (int)sizeof(T);
+  a.xa = (a.ex + align - 1) / align * align;
+  a.wbox = (a.xa + M2_TX + a.ex + align - 1) / align * align;
+  a.hy = M2_TY + 2 * a.ey;
+  CUtensorMap tin;
+  const CUtensorMapDataType dt = sizeof(T) == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_UINT16;
+  if (!make_tmap_3d(&tin, in.p, dt, sizeof(T), in.nx, in.ny, in.nz, a.wbox, a.hy))
+    return cudaErrorNotSupported;
+  a.stage_pitch = (a.hy * a.wbox * (int)sizeof(T) + 127) / 128 * 128;
+  a.off_runs = M2_NST * a.stage_pitch;
+  a.off_bar = a.off_runs + a.n_lens * a.hy * a.wc * 4;
+  a.off_bar = (a.off_bar + 15) / 16 * 16;
+  const int smem = a.off_bar + M2_NST * 8 + 128;
+  if (smem > 110 * 1024) return cudaErrorNotSupported;
+  a.nzi = (int)in.nz;
+  a.zo = (int)zo;
+  a.nzo = (int)nzo;
+  a.nx = (int)in.nx;
+  a.ny = (int)in.ny;
+  const int gx = (int)((in.nx + M2_TX - 1) / M2_TX), gy = (int)((in.ny + M2_TY - 1) / M2_TY);
+  const int64_t tiles = (int64_t)gx * gy;
+  const int64_t want = std::max<int64_t>(1, (2 * 2 * kNumSMs + tiles - 1) / tiles);
+  a.zchunk = (int)std::max<int64_t>(std::min<int64_t>(nzo, 8 * EZ + 8), (nzo + want - 1) / want);
+  dim3 grid(gx, gy, (unsigned)((nzo + a.zchunk - 1) / a.zchunk));
+  auto kern = k_morph2<T, MAX, EZ>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  kern<<<grid, M2_NT, smem, s>>>(tin, (T*)out, a);
+  return cudaGetLastError();
+}
+
+template <typename T, bool MAX>
+cudaError_t dispatch_morph2(const DevIn& in, int64_t zo, int64_t nzo, void* out,
+                            const Morph2Args& a, cudaStream_t s) {
+  switch (a.ez) {
+    case 0: return launch_morph2<T, MAX, 0>(in, zo, nzo, out, a, s);
+    case 1: return launch_morph2<T, MAX, 1>(in, zo, nzo, out, a, s);
+    case 2: return launch_morph2<T, MAX, 2>(in, zo, nzo, out, a, s);
+    case 3: return launch_morph2<T, MAX, 3>(in, zo, nzo, out, a, s);
+    case 4: return launch_morph2<T, MAX, 4>(in, zo, nzo, out, a, s);
+  }
+  return cudaErrorNotSupported;
+}
+
 }  // namespace
 
 cudaError_t morph(const DevIn& in, int64_t zo, int64_t nzo, void* out, const int32_t* offsets,
                   int n, bool is_max, cudaStream_t s, int64_t* launches) {
   if (nzo <= 0) return cudaSuccess;
+  if ((in.dt == HB_U16 || in.dt == HB_U8) && in.nx >= 8 && in.ny >= 8) {
+    Morph2Args a2;
+    if (build_morph2(offsets, n, a2)) {
+      cudaError_t e;
+      if (in.dt == HB_U16)
+        e = is_max ? dispatch_morph2<uint16_t, true>(in, zo, nzo, out, a2, s)
+                   : dispatch_morph2<uint16_t, false>(in, zo, nzo, out, a2, s);
+      else
+        e = is_max ? dispatch_morph2<uint8_t, true>(in, zo, nzo, out, a2, s)
+                   : dispatch_morph2<uint8_t, false>(in, zo, nzo, out, a2, s);
+      if (e != cudaErrorNotSupported) {
+        if (e == cudaSuccess && launches) *launches += 1;
+        return e;
+      }
+      cudaGetLastError();
+    }
+  }
   SeRows se;
   if (!build_rows(offsets, n, se)) return cudaErrorNotSupported;
   switch (in.dt) {
