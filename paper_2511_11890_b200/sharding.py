@@ -1,0 +1,125 @@
+"""Z-slab data parallelism across GPUs with neighbour-only halo exchange.
+
+The reference runs one process and one device (chunks execute
+sequentially, chunking.py:244).  Every hot-path operator is local with a
+finite Z dependence radius (OpProfile.halo_z, chunking.py:75-79), so a volume
+partitioned into contiguous z-slabs — one per rank — is processed
+independently once each rank holds `halo` ghost slices from its neighbours;
+plan invariance makes the stitched result identical to the
+single-device one.
+
+Two ways to obtain the ghost slices:
+
+* host-resident input (``registry.run_operator`` per rank): each rank simply
+  reads its padded range — no collective at all;
+* device-resident, already-sharded input (this module): one
+  ``send/recv`` pair per neighbour and per chained stage over NCCL
+  (NVLink/NVSwitch), i.e. halo slices of stage ``s`` output feed stage ``s+1``.
+
+One process per GPU; ``torch.distributed`` provides the plumbing (``nccl`` on
+B200, ``gloo`` in the CPU tests).  The per-block compute is injected
+(``apply_block``) so the exchange/stitching logic is testable without a GPU;
+the default is the device path (``_native.apply_device``).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Callable, Optional
+
+import numpy as np
+
+
+@dataclass(frozen=True)
+class Slab:
+    """Interior z-range [z0, z1) owned by one rank."""
+
+    rank: int
+    z0: int
+    z1: int
+
+    @property
+    def size(self) -> int:
+        return self.z1 - self.z0
+
+
+def partition(nz: int, world: int) -> list:
+    """Contiguous balanced z-slabs (sizes differ by at most one slice)."""
+    if world < 1 or nz < world:
+        raise ValueError(f"cannot split {nz} slices over {world} ranks")
+    base, extra = divmod(nz, world)
+    out, z = [], 0
+    for r in range(world):
+        n = base + (1 if r < extra else 0)
+        out.append(Slab(r, z, z + n))
+        z += n
+    return out
+
+
+def _dist():
+    import torch.distributed as dist
+
+    return dist
+
+
+def exchange_halos(local, halo: int, rank: int, world: int, group=None):
+    """Return (padded, lo, hi): ``local`` (Zr, Y, X) extended with up to
+    ``halo`` slices received from each neighbour.  ``lo``/``hi`` are the ghost
+    slices actually present (0 at the global faces, where the operator clamps
+    exactly as the reference does at volume faces).
+    """
+    import torch
+
+    if halo == 0 or world == 1:
+        return local, 0, 0
+    if local.shape[0] < halo:
+        raise ValueError(f"slab of {local.shape[0]} slices is thinner than the halo {halo}")
+    dist = _dist()
+    ops = []
+    lo_buf = hi_buf = None
+    if rank > 0:
+        lo_buf = torch.empty((halo,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+        ops.append(dist.P2POp(dist.irecv, lo_buf, rank - 1, group))
+        ops.append(dist.P2POp(dist.isend, local[:halo].contiguous(), rank - 1, group))
+    if rank < world - 1:
+        hi_buf = torch.empty((halo,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+        ops.append(dist.P2POp(dist.isend, local[-halo:].contiguous(), rank + 1, group))
+        ops.append(dist.P2POp(dist.irecv, hi_buf, rank + 1, group))
+    for req in dist.batch_isend_irecv(ops):
+        req.wait()
+    parts = [p for p in (lo_buf, local, hi_buf) if p is not None]
+    padded = torch.cat(parts, dim=0) if len(parts) > 1 else local
+    return padded, (halo if lo_buf is not None else 0), (halo if hi_buf is not None else 0)
+
+
+def _device_apply(block, program, z_begin: int, nz_out: int):
+    import torch
+
+    from . import _native
+
+    out_dt = program.out_dtype(np.dtype(str(block.dtype).replace("torch.", "")))
+    out = torch.empty((nz_out,) + tuple(block.shape[1:]), dtype=getattr(torch, out_dt.name),
+                      device=block.device)
+    _native.apply_device(block, out, program, z_begin)
+    return out
+
+
+def run_sharded(local, program, rank: int, world: int, group=None,
+                apply_block: Optional[Callable] = None, per_stage: bool = True):
+    """Apply ``program`` to a z-sharded volume; returns this rank's interior output.
+
+    per_stage=True: one halo exchange per chained stage (stage s+1's ghosts are
+    stage s outputs), so no slice is computed twice.  per_stage=False: one
+    exchange of the chain's total halo, then the whole chain on the padded slab.
+    """
+    from . import _native
+
+    apply_block = apply_block or _device_apply
+    stages = program.stages if per_stage else [None]
+    cur = local
+    for st in stages:
+        prog = _native.DeviceProgram([st]) if st is not None else program
+        h = prog.halo()
+        padded, lo, hi = exchange_halos(cur, h, rank, world, group)
+        cur = apply_block(padded, prog, lo, padded.shape[0] - lo - hi)
+    return cur
