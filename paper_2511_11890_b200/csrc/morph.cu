@@ -10,6 +10,7 @@
 // output — for ball:3 that is 29 row terms instead of 123 offsets.
 #include <vector>
 #include <algorithm>
+#include <array>
 #include <map>
 
 #include "ops.cuh"
@@ -481,12 +482,331 @@ cudaError_t dispatch_morph2(const DevIn& in, int64_t zo, int64_t nzo, void* out,
   return cudaErrorNotSupported;
 }
 
+
+// ===========================================================================
+// v3: compile-time structuring elements (ball / box / cross, r <= 3) — the fast
+// path for the reference's factory shapes (morphology.py:49-82).
+// ---------------------------------------------------------------------------
+// Layer |dz| of the SE is a 2D shape of centred x-runs with half-width
+// hw(dz, dy) (-1 = row absent), known at compile time.  Per input slice:
+//   H: each (row, 4-wide x block) item builds the run reductions h_k, k<=R,
+//      as packed u16x2 pairs: h_k = op(h_{k-1}, shift(-k), shift(+k)), one
+//      3-input VIMNMX per k, odd shifts via PRMT; stored to smem.
+//   V: each thread folds the rows of every layer for its 4 outputs (two
+//      u16x2 words); identical smem loads across layers are CSE'd.
+//   Z: layer values are pushed into a (2R+1)-slot register ring of pending
+//      outputs (output z takes layer |dz| of slice z+dz); the oldest is stored.
+// u8 volumes are widened into u16 lanes on load and narrowed on store.
+// ===========================================================================
+enum { SE_BALL = 0, SE_BOX = 1, SE_CROSS = 2 };
+
+template <int KIND, int R>
+struct SeShape {
+  static constexpr __host__ __device__ int isqrt(int v) {
+    int r = 0;
+    while ((r + 1) * (r + 1) <= v) ++r;
+    return r;
+  }
+  // half-width of the x-run at (dz, dy), -1 if the row is absent
+  static constexpr __host__ __device__ int hw(int dz, int dy) {
+    if (dz < 0) dz = -dz;
+    if (dy < 0) dy = -dy;
+    if (dz > R || dy > R) return -1;
+    if (KIND == SE_BOX) return R;
+    if (KIND == SE_CROSS) return (dz == 0 && dy == 0) ? R : ((dz == 0 || dy == 0) ? 0 : -1);
+    const int rem = R * R - dz * dz - dy * dy;
+    return rem < 0 ? -1 : isqrt(rem);
+  }
+  static constexpr __host__ __device__ bool needs(int k) {  // is run half-width k used anywhere?
+    for (int dz = 0; dz <= R; ++dz)
+      for (int dy = 0; dy <= R; ++dy)
+        if (hw(dz, dy) == k) return true;
+    return false;
+  }
+};
+
+constexpr int M3X_TX = 64, M3X_TY = 32, M3X_NT = 512, M3X_NST = 3;
+constexpr int M3X_Q = M3X_TX / 4;  // 4-wide x blocks per row (16)
+
+struct Morph3Args {
+  int nzi, zo, nzo, zchunk, nx, ny;
+};
+
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t d;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+  return d;
+}
+template <bool MAX>
+__device__ __forceinline__ uint32_t op3x2(uint32_t a, uint32_t b, uint32_t c) {
+  return op2x2<MAX>(op2x2<MAX>(a, b), c);  // ptxas fuses into VIMNMX3.U16x2
+}
+
+template <typename T, bool MAX, int KIND, int R>
+__global__ void __launch_bounds__(M3X_NT, 2)
+k_morph3(const __grid_constant__ CUtensorMap tin, T* __restrict__ out, const Morph3Args a) {
+  using S = SeShape<KIND, R>;
+  constexpr int ALIGN = 16 / (int)sizeof(T);
+  constexpr int XA = (R + ALIGN - 1) / ALIGN * ALIGN < 4 ? 4 : (R + ALIGN - 1) / ALIGN * ALIGN;
+  constexpr int XA2 = (XA + ALIGN - 1) / ALIGN * ALIGN;   // box start offset (>= 4, 16-B aligned)
+  constexpr int WBOX = (XA2 + M3X_TX + XA2 + ALIGN - 1) / ALIGN * ALIGN;
+  constexpr int HY = M3X_TY + 2 * R;
+  constexpr int STAGE_BYTES = HY * WBOX * (int)sizeof(T);
+  constexpr int STAGE_PITCH = (STAGE_BYTES + 127) / 128 * 128;
+  constexpr int RING = 2 * R + 1;
+  constexpr int WPR = M3X_TX / 2;  // u16x2 words per H row (32)
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem =
+      reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~(uintptr_t)127);
+  T* sraw = reinterpret_cast<T*>(smem);
+  uint32_t* sH = reinterpret_cast<uint32_t*>(smem + M3X_NST * STAGE_PITCH);  // [R][HY][WPR]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + M3X_NST * STAGE_PITCH + (R > 0 ? R : 1) * HY * WPR * 4);
+  const int tid = threadIdx.x;
+  const int x0 = blockIdx.x * M3X_TX, y0 = blockIdx.y * M3X_TY;
+  const int z0 = blockIdx.z * a.zchunk;
+  const int z1 = min(z0 + a.zchunk, a.nzo);
+  const int nsl = (z1 - z0) + 2 * R;
+  const bool border = (x0 - R < 0) || (x0 + M3X_TX + R > a.nx) || (y0 - R < 0) || (y0 + M3X_TY + R > a.ny);
+  constexpr uint32_t BOX_BYTES = HY * WBOX * sizeof(T);
+  auto zin_of = [&](int s) { return min(max(a.zo + z0 - R + s, 0), a.nzi - 1); };
+
+  if (tid == 0) {
+    prefetch_tmap(&tin);
+    for (int i = 0; i < M3X_NST; ++i) mbar_init(&bar[i], 1);
+    fence_mbar_init();
+    for (int i = 0; i < M3X_NST && i < nsl; ++i) {
+      mbar_expect_tx(&bar[i], BOX_BYTES);
+      tma_load_3d(sraw + i * (STAGE_PITCH / sizeof(T)), &tin, x0 - XA2, y0 - R, zin_of(i), &bar[i]);
+    }
+  }
+  __syncthreads();
+
+  // V/Z ownership: row vy, 4-wide x block vq (two u16x2 words: pairs 2vq, 2vq+1)
+  const int vq = tid % M3X_Q, vy = tid / M3X_Q;  // vy in [0, 32)
+  uint32_t acc[RING][2];
+  constexpr uint32_t IDENT = MAX ? 0u : 0xffffffffu;
+#pragma unroll
+  for (int u = 0; u < RING; ++u) acc[u][0] = acc[u][1] = IDENT;
+
+  // load the u16x2 word covering x = (tile) 2p, 2p+1 of stage row r
+  auto word = [&](const T* row, int p) -> uint32_t {
+    if constexpr (sizeof(T) == 2) {
+      return *reinterpret_cast<const uint32_t*>(row + XA2 + 2 * p);
+    } else {
+      const uint16_t b2 = *reinterpret_cast<const uint16_t*>(row + XA2 + 2 * p);
+      return (uint32_t)(b2 & 0xff) | ((uint32_t)(b2 >> 8) << 16);
+    }
+  };
+
+  for (int s = 0; s < nsl; ++s) {
+    const int st = s % M3X_NST;
+    T* stage = sraw + st * (STAGE_PITCH / sizeof(T));
+    mbar_wait(&bar[st], (uint32_t)((s / M3X_NST) & 1));
+    if (border) {
+      constexpr int WC = M3X_TX + 2 * XA2;
+      for (int e = tid; e < HY * WC; e += M3X_NT) {
+        const int ly = e / WC, lx = e - ly * WC;
+        const int gy = y0 - R + ly, gx = x0 - XA2 + lx;
+        const int cy = min(max(gy, 0), a.ny - 1), cx = min(max(gx, 0), a.nx - 1);
+        if (cy != gy || cx != gx) stage[ly * WBOX + lx] = stage[(cy - (y0 - R)) * WBOX + (cx - (x0 - XA2))];
+      }
+      fence_proxy_async();
+      __syncthreads();
+    }
+    // ---- H: run reductions for every halo'd row -----------------------------
+    if constexpr (R > 0) {
+      for (int item = tid; item < HY * M3X_Q; item += M3X_NT) {
+        const int r = item / M3X_Q, q = item % M3X_Q;
+        const T* row = stage + r * WBOX;
+        uint32_t w[6];  // pairs 2q-2 .. 2q+3
+#pragma unroll
+        for (int i = 0; i < 6; ++i) w[i] = word(row, 2 * q - 2 + i);
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {  // pair 2q + j -> w[2 + j]
+          const uint32_t c = w[2 + j];
+          // shift(d): the pair of voxels (2j+d, 2j+d+1) relative to x = 4q; word i
+          // holds voxels (2i-4, 2i-3); odd starts straddle two words
+          auto sh = [&](int d) -> uint32_t {
+            const int v = 2 * j + d;
+            if ((v & 1) == 0) return w[(v + 4) / 2];
+            const int k = (v + 3) / 2;
+            return prmt(w[k], w[k + 1], 0x5432);
+          };
+          uint32_t h = c;
+#pragma unroll
+          for (int k = 1; k <= R; ++k) {
+            h = op3x2<MAX>(h, sh(-k), sh(k));
+            if (S::needs(k)) sH[((k - 1) * HY + r) * WPR + 2 * q + j] = h;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    // ---- V: every layer's 2D shape for this thread's 4 outputs ----------------
+    uint32_t layer[R + 1][2];
+#pragma unroll
+    for (int L = 0; L <= R; ++L) {
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        uint32_t v = IDENT;
+#pragma unroll
+        for (int dy = -R; dy <= R; ++dy) {
+          const int k = S::hw(L, dy);
+          if (k < 0) continue;
+          const int r = vy + R + dy;
+          uint32_t t;
+          if (k == 0) t = word(stage + r * WBOX, 2 * vq + j);
+          else t = sH[((k - 1) * HY + r) * WPR + 2 * vq + j];
+          v = op2x2<MAX>(v, t);
+        }
+        layer[L][j] = v;
+      }
+    }
+    // ---- Z: push into the ring; output z = s - 2R completes -------------------
+    switch (s % RING) {
+#define HB_M3_CASE(U)                                                                   \
+  case U:                                                                               \
+    if constexpr (U < RING) {                                                           \
+      _Pragma("unroll") for (int d = -R; d <= R; ++d) {                                 \
+        constexpr int dummy = 0; (void)dummy;                                           \
+        const int slot = ((U - d) % RING + RING) % RING;                                \
+        const int L = d < 0 ? -d : d;                                                   \
+        acc[slot][0] = op2x2<MAX>(acc[slot][0], layer[L][0]);                           \
+        acc[slot][1] = op2x2<MAX>(acc[slot][1], layer[L][1]);                           \
+      }                                                                                 \
+      {                                                                                 \
+        const int o = s - 2 * R;                                                        \
+        constexpr int slot = ((U - R) % RING + RING) % RING;                            \
+        if (o >= 0) {                                                                   \
+          const int gy = y0 + vy, gx = x0 + 4 * vq;                                     \
+          if (gy < a.ny && gx < a.nx) {                                                 \
+            T* dst = out + ((int64_t)(z0 + o) * a.ny + gy) * (int64_t)a.nx + gx;         \
+            const uint32_t v0 = acc[slot][0], v1 = acc[slot][1];                        \
+            if (gx + 3 < a.nx) {                                                        \
+              if constexpr (sizeof(T) == 2) {                                           \
+                *reinterpret_cast<uint2*>(dst) = make_uint2(v0, v1);                    \
+              } else {                                                                  \
+                *reinterpret_cast<uint32_t*>(dst) = prmt(v0, v1, 0x6420);               \
+              }                                                                         \
+            } else {                                                                    \
+              const uint32_t vv[2] = {v0, v1};                                          \
+              for (int i = 0; i < 4 && gx + i < a.nx; ++i)                              \
+                dst[i] = (T)((vv[i >> 1] >> (16 * (i & 1))) & 0xffffu);                  \
+            }                                                                           \
+          }                                                                             \
+        }                                                                               \
+        acc[slot][0] = acc[slot][1] = IDENT;                                            \
+      }                                                                                 \
+    }                                                                                   \
+    break;
+      HB_M3_CASE(0) HB_M3_CASE(1) HB_M3_CASE(2) HB_M3_CASE(3) HB_M3_CASE(4) HB_M3_CASE(5) HB_M3_CASE(6)
+#undef HB_M3_CASE
+      default: break;
+    }
+    __syncthreads();  // sH and this stage (raw rows read by V) are free again
+    if (tid == 0 && s + M3X_NST < nsl) {
+      fence_proxy_async();
+      mbar_expect_tx(&bar[st], BOX_BYTES);
+      tma_load_3d(stage, &tin, x0 - XA2, y0 - R, zin_of(s + M3X_NST), &bar[st]);
+    }
+  }
+}
+
+// Recognise the factory shapes from an offset list (exact set equality).
+bool classify_se(const int32_t* off, int n, int& kind, int& r) {
+  std::vector<std::array<int, 3>> v(n);
+  int ext = 0;
+  for (int k = 0; k < n; ++k) {
+    v[k] = {off[3 * k], off[3 * k + 1], off[3 * k + 2]};
+    ext = std::max({ext, std::abs(v[k][0]), std::abs(v[k][1]), std::abs(v[k][2])});
+  }
+  std::sort(v.begin(), v.end());
+  v.erase(std::unique(v.begin(), v.end()), v.end());
+  if (ext < 1 || ext > 3) return false;
+  for (int kd = 0; kd < 3; ++kd) {
+    std::vector<std::array<int, 3>> w;
+    for (int dz = -ext; dz <= ext; ++dz)
+      for (int dy = -ext; dy <= ext; ++dy)
+        for (int dx = -ext; dx <= ext; ++dx) {
+          bool in;
+          if (kd == SE_BOX) in = true;
+          else if (kd == SE_BALL) in = dz * dz + dy * dy + dx * dx <= ext * ext;
+          else in = (dz == 0 && dy == 0) || (dz == 0 && dx == 0) || (dy == 0 && dx == 0);
+          if (in) w.push_back({dz, dy, dx});
+        }
+    if (w == v) {
+      kind = kd;
+      r = ext;
+      return true;
+    }
+  }
+  return false;
+}
+
+template <typename T, bool MAX, int KIND, int R>
+cudaError_t launch_morph3(const DevIn& in, int64_t zo, int64_t nzo, void* out, cudaStream_t s) {
+  constexpr int ALIGN = 16 / (int)sizeof(T);
+  constexpr int XA = (R + ALIGN - 1) / ALIGN * ALIGN < 4 ? 4 : (R + ALIGN - 1) / ALIGN * ALIGN;
+  constexpr int XA2 = (XA + ALIGN - 1) / ALIGN * ALIGN;
+  constexpr int WBOX = (XA2 + M3X_TX + XA2 + ALIGN - 1) / ALIGN * ALIGN;
+  constexpr int HY = M3X_TY + 2 * R;
+  constexpr int STAGE_PITCH = (HY * WBOX * (int)sizeof(T) + 127) / 128 * 128;
+  const int smem = M3X_NST * STAGE_PITCH + R * HY * (M3X_TX / 2) * 4 + M3X_NST * 8 + 128;
+  CUtensorMap tin;
+  const CUtensorMapDataType dt = sizeof(T) == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_UINT16;
+  if (!make_tmap_3d(&tin, in.p, dt, sizeof(T), in.nx, in.ny, in.nz, WBOX, HY)) return cudaErrorNotSupported;
+  Morph3Args a;
+  a.nzi = (int)in.nz;
+  a.zo = (int)zo;
+  a.nzo = (int)nzo;
+  a.nx = (int)in.nx;
+  a.ny = (int)in.ny;
+  const int gx = (int)((in.nx + M3X_TX - 1) / M3X_TX), gy = (int)((in.ny + M3X_TY - 1) / M3X_TY);
+  const int64_t tiles = (int64_t)gx * gy;
+  const int64_t want = std::max<int64_t>(1, (4 * kNumSMs + tiles - 1) / tiles);
+  a.zchunk = (int)std::max<int64_t>(std::min<int64_t>(nzo, 8 * R + 8), (nzo + want - 1) / want);
+  dim3 grid(gx, gy, (unsigned)((nzo + a.zchunk - 1) / a.zchunk));
+  auto kern = k_morph3<T, MAX, KIND, R>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  kern<<<grid, M3X_NT, smem, s>>>(tin, (T*)out, a);
+  return cudaGetLastError();
+}
+
+template <typename T, bool MAX>
+cudaError_t dispatch_morph3(int kind, int r, const DevIn& in, int64_t zo, int64_t nzo, void* out,
+                            cudaStream_t s) {
+#define HB_M3_K(K)                                                              \
+  if (kind == K) {                                                              \
+    if (r == 1) return launch_morph3<T, MAX, K, 1>(in, zo, nzo, out, s);        \
+    if (r == 2) return launch_morph3<T, MAX, K, 2>(in, zo, nzo, out, s);        \
+    if (r == 3) return launch_morph3<T, MAX, K, 3>(in, zo, nzo, out, s);        \
+  }
+  HB_M3_K(SE_BALL) HB_M3_K(SE_BOX) HB_M3_K(SE_CROSS)
+#undef HB_M3_K
+  return cudaErrorNotSupported;
+}
+
 }  // namespace
 
 cudaError_t morph(const DevIn& in, int64_t zo, int64_t nzo, void* out, const int32_t* offsets,
                   int n, bool is_max, cudaStream_t s, int64_t* launches) {
   if (nzo <= 0) return cudaSuccess;
   if ((in.dt == HB_U16 || in.dt == HB_U8) && in.nx >= 8 && in.ny >= 8) {
+    int kind = 0, rr = 0;
+    if (classify_se(offsets, n, kind, rr)) {
+      cudaError_t e;
+      if (in.dt == HB_U16)
+        e = is_max ? dispatch_morph3<uint16_t, true>(kind, rr, in, zo, nzo, out, s)
+                   : dispatch_morph3<uint16_t, false>(kind, rr, in, zo, nzo, out, s);
+      else
+        e = is_max ? dispatch_morph3<uint8_t, true>(kind, rr, in, zo, nzo, out, s)
+                   : dispatch_morph3<uint8_t, false>(kind, rr, in, zo, nzo, out, s);
+      if (e != cudaErrorNotSupported) {
+        if (e == cudaSuccess && launches) *launches += 1;
+        return e;
+      }
+      cudaGetLastError();
+    }
     Morph2Args a2;
     if (build_morph2(offsets, n, a2)) {
       cudaError_t e;

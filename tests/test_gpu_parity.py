@@ -250,3 +250,19 @@ def test_large_slab_sampled_median(hb, oracle):
         lo, hi = max(0, z0 - 1), min(64, z0 + 2)
         ref = oracle.median(x[lo:hi], 1)
         assert np.array_equal(got[z0], ref[z0 - lo])
+
+
+@pytest.mark.parametrize("dt", ["u16", "u8", "bin"])
+def test_factory_se_fast_path(hb, oracle, dt):
+    """The compile-time SE kernels (ball/box/cross r<=3) on tile-aligned and
+    ragged shapes, erosion and dilation, bit-exact."""
+    from paper_2511_11890_b200 import morphology
+
+    rng = np.random.default_rng(11)
+    for shape in [(12, 64, 128), (9, 33, 70), (5, 64, 64)]:
+        x = _vol(rng, shape, dt)
+        for kind in ("ball", "box", "cross"):
+            for r in (1, 2, 3):
+                s = morphology.StructuringElement.parse(f"{kind}:{r}")
+                assert np.array_equal(morphology.erode(x, s), oracle.erode(x, s.offsets)), (shape, kind, r)
+                assert np.array_equal(morphology.dilate(x, s), oracle.dilate(x, s.offsets)), (shape, kind, r)
