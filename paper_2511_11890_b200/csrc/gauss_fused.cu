@@ -107,8 +107,8 @@ struct Geo {
   static constexpr int WBOX = (XA + TX + R + ALIGN - 1) / ALIGN * ALIGN;  // smem row pitch
   static constexpr int STAGE_BYTES = HB * WBOX * (int)sizeof(Tin);
   static constexpr int STAGE_PITCH = (STAGE_BYTES + 127) / 128 * 128;
-  static constexpr int NST = R <= 3 ? 6 : 3;                            // TMA ring depth
-  static constexpr int MINB = R <= 3 ? 2 : 1;                           // CTAs per SM
+  static constexpr int NST = R <= 1 ? 4 : (R <= 3 ? 6 : 3);            // TMA ring depth
+  static constexpr int MINB = R <= 1 ? 3 : (R <= 3 ? 2 : 1);           // CTAs per SM
   static constexpr int RING = 2 * R + 1;
   static constexpr int SY_BYTES = 2 * TY * SY_STRIDE * 4;
   static constexpr int SOUT_BYTES = 2 * TY * TX * 4;
