@@ -700,7 +700,7 @@ int32_t hb_run(const hb_volume* in, hb_volume* out, const hb_stage* stages, int3
   }
   // validate the plan: interiors must partition [0, Z), halos within the volume
   int64_t expect = 0;
-  int64_t max_pad = 0, max_int = 0;
+  int64_t max_int = 0;
   for (int64_t k = 0; k < nchunks; k++) {
     const hb_chunk& c = chunks[k];
     if (c.z_start != expect || c.z_stop <= c.z_start || c.halo_lo < 0 || c.halo_hi < 0 ||
@@ -709,7 +709,6 @@ int32_t hb_run(const hb_volume* in, hb_volume* out, const hb_stage* stages, int3
       return HB_EPARAM;
     }
     expect = c.z_stop;
-    max_pad = std::max(max_pad, c.z_stop - c.z_start + c.halo_lo + c.halo_hi);
     max_int = std::max(max_int, c.z_stop - c.z_start);
   }
   if (expect != in->nz) {
@@ -730,33 +729,58 @@ int32_t hb_run(const hb_volume* in, hb_volume* out, const hb_stage* stages, int3
   }
   const size_t plane = (size_t)in->ny * in->nx;
   const size_t in_es = dtype_size(in->dtype), out_es = dtype_size(out->dtype);
-  // worst-case per-slot device bytes: padded input slab + interior output + chain scratch
-  size_t scratch = 0;
-  for (int64_t k = 0; k < nchunks; k++) {
-    const hb_chunk& c = chunks[k];
-    int64_t pn = c.z_stop - c.z_start + c.halo_lo + c.halo_hi;
-    scratch = std::max(scratch, chain_scratch(st, pn, in->ny, in->nx, c.halo_lo,
-                                              c.z_stop - c.z_start));
-  }
-  const size_t slot_bytes = (size_t)max_pad * plane * in_es + (size_t)max_int * plane * out_es + scratch;
-  int depth = ex->pipeline_depth > 0 ? ex->pipeline_depth : 2;
-  depth = (int)std::min<int64_t>(depth, std::max<int64_t>(1, nchunks));
+  int64_t H = 0;
+  for (auto& d : st) H += d.halo;
+
+  // ---- pieces: every plan chunk is streamed as z-pieces of <= S interior
+  // slices.  A piece's padded block is clamped to its chunk's padded block, so
+  // each piece reproduces the chunk-level (reference) result exactly; pieces
+  // bound the device working set and deepen the copy/compute overlap.
+  auto slot_bytes_for = [&](int64_t S) -> size_t {
+    const int64_t pad = S + 2 * H;
+    return (size_t)pad * plane * in_es + (size_t)S * plane * out_es +
+           chain_scratch(st, pad, in->ny, in->nx, H, S);
+  };
   size_t free_b = 0, total_b = 0;
   cudaMemGetInfo(&free_b, &total_b);
   // Hard limit: physically free device memory.  Soft target: the job budget
-  // (the planner's scratch factors are the reference's host estimates, so a
-  // plan the reference accepts must never fail here just because the device
-  // layout differs; we drop to a serial pipeline first).
-  size_t cap = free_b > (256u << 20) ? free_b - (256u << 20) : 0;
+  // (the planner's scratch factors are the reference's host estimates; a plan
+  // the reference accepts must not fail here just because the device layout
+  // differs, so pieces shrink and the pipeline gets shallower first).
+  const size_t cap = free_b > (256u << 20) ? free_b - (256u << 20) : 0;
   size_t soft = cap;
   if (ex->device_budget > 0) soft = std::min(cap, (size_t)ex->device_budget);
-  while (depth > 1 && (size_t)depth * slot_bytes > soft) depth--;
-  if (slot_bytes > cap) {
-    rep->minimum_bytes = (int64_t)slot_bytes;
+  const size_t target = (size_t)160 << 20;  // ~160 MiB per pipeline slot
+  int64_t S = max_int;
+  while (S > 1 && slot_bytes_for(S) > target && S > 2 * H) S = std::max<int64_t>(1, S * 3 / 4);
+  int depth = ex->pipeline_depth > 0 ? ex->pipeline_depth : 3;
+  while (depth > 1 && (size_t)depth * slot_bytes_for(S) > soft) depth--;
+  while (S > 1 && slot_bytes_for(S) > soft) S = std::max<int64_t>(1, S / 2);
+  if (slot_bytes_for(S) > cap) {
+    rep->minimum_bytes = (int64_t)slot_bytes_for(S);
     set_err(rep, "device budget of " + std::to_string(cap) + " bytes cannot hold one chunk (" +
-                     std::to_string(slot_bytes) + " bytes needed)");
+                     std::to_string(slot_bytes_for(S)) + " bytes needed)");
     return HB_EBUDGET_SMALL;
   }
+  struct Piece {
+    int64_t chunk, a, b, p0, p1;
+  };
+  std::vector<Piece> pieces;
+  std::vector<int64_t> last_piece(nchunks, -1);
+  int64_t max_pad = 0;
+  for (int64_t k = 0; k < nchunks; k++) {
+    const hb_chunk& c = chunks[k];
+    const int64_t cs = c.z_start - c.halo_lo, ce = c.z_stop + c.halo_hi;
+    for (int64_t a0 = c.z_start; a0 < c.z_stop; a0 += S) {
+      const int64_t b0 = std::min(a0 + S, c.z_stop);
+      Piece pc{k, a0, b0, std::max(cs, a0 - H), std::min(ce, b0 + H)};
+      max_pad = std::max(max_pad, pc.p1 - pc.p0);
+      last_piece[k] = (int64_t)pieces.size();
+      pieces.push_back(pc);
+    }
+  }
+  const int64_t npieces = (int64_t)pieces.size();
+  depth = (int)std::min<int64_t>(depth, std::max<int64_t>(1, npieces));
   const int threads = auto_threads(ex->host_threads);
   const bool in_pinned = is_pinned(in->data), out_pinned = is_pinned(out->data);
   PinnedRing& ring = g_ring[dev];
@@ -772,14 +796,13 @@ int32_t hb_run(const hb_volume* in, hb_volume* out, const hb_stage* stages, int3
   cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking);
   cudaStreamCreateWithFlags(&s_comp, cudaStreamNonBlocking);
   cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking);
-  std::vector<cudaEvent_t> ev_h2d(depth), ev_comp(depth), ev_d2h(depth), ev_k0(depth);
+  std::vector<cudaEvent_t> ev_h2d(depth), ev_comp(depth), ev_k0(depth);
   for (int i = 0; i < depth; i++) {
     cudaEventCreate(&ev_h2d[i]);
     cudaEventCreate(&ev_comp[i]);
-    cudaEventCreate(&ev_d2h[i]);
     cudaEventCreate(&ev_k0[i]);
   }
-  std::vector<cudaEvent_t> ev_done(nchunks);
+  std::vector<cudaEvent_t> ev_done(npieces);
   for (auto& v : ev_done) cudaEventCreate(&v);
   cudaEvent_t ev_start;
   cudaEventCreate(&ev_start);
@@ -787,13 +810,11 @@ int32_t hb_run(const hb_volume* in, hb_volume* out, const hb_stage* stages, int3
   pool_reset_peak(dev);
   std::vector<PoolAlloc> slots;
   std::vector<void*> dbuf_in(depth), dbuf_out(depth);
-  for (int i = 0; i < depth; i++) {
-    slots.push_back(PoolAlloc{g_dev[dev].pool, s_comp});
-  }
+  for (int i = 0; i < depth; i++) slots.push_back(PoolAlloc{g_dev[dev].pool, s_comp});
   PoolAlloc io{g_dev[dev].pool, s_comp};
   for (int i = 0; i < depth && e == cudaSuccess; i++) {
     dbuf_in[i] = io.get((size_t)max_pad * plane * in_es);
-    dbuf_out[i] = io.get((size_t)max_int * plane * out_es);
+    dbuf_out[i] = io.get((size_t)S * plane * out_es);
     if (!dbuf_in[i] || !dbuf_out[i]) e = io.err;
   }
   if (e == cudaSuccess) e = cudaStreamSynchronize(s_comp);
@@ -802,7 +823,7 @@ int32_t hb_run(const hb_volume* in, hb_volume* out, const hb_stage* stages, int3
     cudaStreamSynchronize(s_comp);
     cudaGetLastError();
     cudaMemPoolTrimTo(g_dev[dev].pool, 0);
-    rep->minimum_bytes = (int64_t)slot_bytes;
+    rep->minimum_bytes = (int64_t)slot_bytes_for(S);
     set_err(rep, std::string("device allocation failed: ") + cudaGetErrorString(e));
     return HB_EBUDGET_SMALL;
   }
@@ -810,110 +831,121 @@ int32_t hb_run(const hb_volume* in, hb_volume* out, const hb_stage* stages, int3
   hb_status status = HB_OK;
   int64_t launches = 0;
   double kernel_ms = 0;
-  std::vector<int64_t> slot_chunk(depth, -1);
+  std::vector<int64_t> slot_piece(depth, -1);
   cudaEventRecord(ev_start, s_in);
 
-  // finish chunk k: its D2H into pageable memory (if needed) and bookkeeping
-  auto finish = [&](int64_t k) -> cudaError_t {
-    int slot = (int)(k % depth);
-    const hb_chunk& c = chunks[k];
-    int64_t n = c.z_stop - c.z_start;
-    size_t bytes = (size_t)n * plane * out_es;
-    char* host_dst = (char*)out->data + (size_t)c.z_start * plane * out_es;
+  // finish piece j: its D2H into pageable memory (if needed) and bookkeeping
+  auto finish = [&](int64_t j) -> cudaError_t {
+    const int slot = (int)(j % depth);
+    const Piece& pc = pieces[j];
+    const size_t bytes = (size_t)(pc.b - pc.a) * plane * out_es;
+    char* host_dst = (char*)out->data + (size_t)pc.a * plane * out_es;
     cudaError_t err = cudaSuccess;
     if (!out_pinned) {
       cudaStreamWaitEvent(s_out, ev_comp[slot], 0);
       err = d2h_staged(ring, host_dst, dbuf_out[slot], bytes, s_out, threads);
-      cudaEventRecord(ev_d2h[slot], s_out);
-      cudaEventRecord(ev_done[k], s_out);
+      cudaEventRecord(ev_done[j], s_out);
     }
-    cudaEventSynchronize(ev_done[k]);
+    cudaEventSynchronize(ev_done[j]);
     float ms = 0;
     if (cudaEventElapsedTime(&ms, ev_k0[slot], ev_comp[slot]) == cudaSuccess) kernel_ms += ms;
     rep->d2h_bytes += (int64_t)bytes;
-    slot_chunk[slot] = -1;
+    slot_piece[slot] = -1;
     return err == cudaSuccess ? cudaGetLastError() : err;
   };
 
-  int64_t k = 0;
-  for (; k < nchunks; k++) {
-    const int slot = (int)(k % depth);
-    if (ex->cancel && ex->cancel(ex->cancel_ctx)) {
-      status = HB_ECANCELLED;
-      set_err(rep, "cancelled before chunk " + std::to_string(k));
-      break;
+  int64_t j = 0;
+  int64_t chunk_now = -1;
+  int64_t prev_p0 = 0, prev_p1 = 0;
+  int prev_slot = -1;
+  for (; j < npieces; j++) {
+    const Piece& pc = pieces[j];
+    const int slot = (int)(j % depth);
+    if (pc.chunk != chunk_now) {  // chunk boundary: cancel poll + fault hook
+      chunk_now = pc.chunk;
+      if (ex->cancel && ex->cancel(ex->cancel_ctx)) {
+        status = HB_ECANCELLED;
+        set_err(rep, "cancelled before chunk " + std::to_string(chunk_now));
+        break;
+      }
+      if (ex->fault_chunk >= 0 && chunk_now == ex->fault_chunk) {
+        status = HB_ECHUNK;
+        set_err(rep, "injected fault on chunk " + std::to_string(chunk_now));
+        break;
+      }
     }
-    if (slot_chunk[slot] >= 0) {
-      e = finish(slot_chunk[slot]);
+    if (slot_piece[slot] >= 0) {
+      e = finish(slot_piece[slot]);
       if (e != cudaSuccess) break;
     }
-    if (ex->fault_chunk >= 0 && k == ex->fault_chunk) {
-      status = HB_ECHUNK;
-      set_err(rep, "injected fault on chunk " + std::to_string(k));
-      break;
+    // input: reuse the overlap with the previous piece's slab on the device
+    // (halo slices cross PCIe once), upload the rest
+    int64_t up0 = pc.p0;
+    if (prev_slot >= 0 && prev_slot != slot && pc.p0 >= prev_p0 && pc.p0 < prev_p1) {
+      const int64_t keep = std::min(prev_p1, pc.p1) - pc.p0;
+      e = cudaMemcpyAsync(dbuf_in[slot], (char*)dbuf_in[prev_slot] + (size_t)(pc.p0 - prev_p0) * plane * in_es,
+                          (size_t)keep * plane * in_es, cudaMemcpyDeviceToDevice, s_in);
+      if (e != cudaSuccess) break;
+      up0 = pc.p0 + keep;
     }
-    const hb_chunk& c = chunks[k];
-    const int64_t ps = c.z_start - c.halo_lo;
-    const int64_t pn = c.z_stop + c.halo_hi - ps;
-    const int64_t n = c.z_stop - c.z_start;
-    const size_t in_bytes = (size_t)pn * plane * in_es;
-    const char* host_src = (const char*)in->data + (size_t)ps * plane * in_es;
-    // H2D (input buffer of this slot is free: its previous compute finished in finish())
-    if (in_pinned) {
-      e = cudaMemcpyAsync(dbuf_in[slot], host_src, in_bytes, cudaMemcpyHostToDevice, s_in);
-    } else {
-      e = h2d_staged(ring, dbuf_in[slot], host_src, in_bytes, s_in, threads);
+    if (up0 < pc.p1) {
+      const size_t bytes = (size_t)(pc.p1 - up0) * plane * in_es;
+      char* dst = (char*)dbuf_in[slot] + (size_t)(up0 - pc.p0) * plane * in_es;
+      const char* src = (const char*)in->data + (size_t)up0 * plane * in_es;
+      e = in_pinned ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s_in)
+                    : h2d_staged(ring, dst, src, bytes, s_in, threads);
+      if (e != cudaSuccess) break;
+      rep->h2d_bytes += (int64_t)bytes;
     }
-    if (e != cudaSuccess) break;
     cudaEventRecord(ev_h2d[slot], s_in);
-    rep->h2d_bytes += (int64_t)in_bytes;
+    prev_p0 = pc.p0;
+    prev_p1 = pc.p1;
+    prev_slot = slot;
     // compute
     cudaStreamWaitEvent(s_comp, ev_h2d[slot], 0);
     cudaEventRecord(ev_k0[slot], s_comp);
-    slots[slot].s = s_comp;
-    DevIn din{dbuf_in[slot], in->dtype, pn, in->ny, in->nx};
-    e = run_chain(st, din, c.halo_lo, n, dbuf_out[slot], slots[slot], s_comp, &launches);
+    DevIn din{dbuf_in[slot], in->dtype, pc.p1 - pc.p0, in->ny, in->nx};
+    e = run_chain(st, din, pc.a - pc.p0, pc.b - pc.a, dbuf_out[slot], slots[slot], s_comp, &launches);
     slots[slot].release();
     if (e != cudaSuccess) break;
     cudaEventRecord(ev_comp[slot], s_comp);
-    // D2H straight into pinned output
     if (out_pinned) {
       cudaStreamWaitEvent(s_out, ev_comp[slot], 0);
-      char* host_dst = (char*)out->data + (size_t)c.z_start * plane * out_es;
-      e = cudaMemcpyAsync(host_dst, dbuf_out[slot], (size_t)n * plane * out_es,
+      char* host_dst = (char*)out->data + (size_t)pc.a * plane * out_es;
+      e = cudaMemcpyAsync(host_dst, dbuf_out[slot], (size_t)(pc.b - pc.a) * plane * out_es,
                           cudaMemcpyDeviceToHost, s_out);
       if (e != cudaSuccess) break;
-      cudaEventRecord(ev_d2h[slot], s_out);
-      cudaEventRecord(ev_done[k], s_out);
+      cudaEventRecord(ev_done[j], s_out);
     }
-    slot_chunk[slot] = k;
+    slot_piece[slot] = j;
   }
-  // drain outstanding chunks in order
+  // drain outstanding pieces in order
   if (status == HB_OK && e == cudaSuccess) {
-    for (int64_t j = std::max<int64_t>(0, k - depth); j < k; j++) {
-      int slot = (int)(j % depth);
-      if (slot_chunk[slot] == j) {
-        e = finish(j);
+    for (int64_t q = std::max<int64_t>(0, j - depth); q < j; q++) {
+      const int slot = (int)(q % depth);
+      if (slot_piece[slot] == q) {
+        e = finish(q);
         if (e != cudaSuccess) break;
       }
     }
   }
   cudaError_t sync_e = cudaDeviceSynchronize();
   if (e == cudaSuccess && status == HB_OK && sync_e != cudaSuccess) e = sync_e;
+  const int64_t at_chunk = j < npieces ? pieces[j].chunk : nchunks - 1;
   if (e != cudaSuccess && status == HB_OK) {
     status = HB_ECUDA;
-    rep->failed_chunk = std::min<int64_t>(k, nchunks - 1);
-    set_err(rep, std::string("CUDA error on chunk ") + std::to_string(rep->failed_chunk) + ": " +
+    rep->failed_chunk = at_chunk;
+    set_err(rep, std::string("CUDA error on chunk ") + std::to_string(at_chunk) + ": " +
                      cudaGetErrorString(e));
     cudaGetLastError();
   } else if (status != HB_OK) {
-    rep->failed_chunk = k;
+    rep->failed_chunk = at_chunk;
   }
   if (status == HB_OK && ex->chunk_seconds) {
-    for (int64_t j = 0; j < nchunks; j++) {
+    for (int64_t k = 0; k < nchunks; k++) {
       float ms = 0;
-      cudaEventElapsedTime(&ms, j == 0 ? ev_start : ev_done[j - 1], ev_done[j]);
-      ex->chunk_seconds[j] = ms * 1e-3;
+      cudaEventElapsedTime(&ms, k == 0 ? ev_start : ev_done[last_piece[k - 1]], ev_done[last_piece[k]]);
+      ex->chunk_seconds[k] = ms * 1e-3;
     }
   }
   for (auto& sl : slots) sl.release();
@@ -925,7 +957,6 @@ int32_t hb_run(const hb_volume* in, hb_volume* out, const hb_stage* stages, int3
   for (int i = 0; i < depth; i++) {
     cudaEventDestroy(ev_h2d[i]);
     cudaEventDestroy(ev_comp[i]);
-    cudaEventDestroy(ev_d2h[i]);
     cudaEventDestroy(ev_k0[i]);
   }
   for (auto& v : ev_done) cudaEventDestroy(v);

@@ -189,7 +189,8 @@ def test_pinned_and_pageable_paths_agree(hb):
     a, ra = registry.run_operator(x, "median", {"radius": 1}, b)
     c, rc = registry.run_operator(pinned, "median", {"radius": 1}, b)
     assert np.array_equal(a, c) and ra.chunk_count == rc.chunk_count >= 5
-    assert ra.h2d_bytes == rc.h2d_bytes > x.nbytes  # halos are re-uploaded per chunk
+    # device z-ring: halo slices are reused on the device, every input byte crosses PCIe once
+    assert ra.h2d_bytes == rc.h2d_bytes == x.nbytes
 
 
 def test_torch_device_blocks(hb, oracle):
