@@ -308,6 +308,11 @@ cudaError_t run_stage(const StageDesc& d, const DevIn& in, int64_t zo, int64_t n
       }
       float* tmp = (float*)pa.get((size_t)nzo * plane * 4);
       if (!tmp) return pa.err;
+      if (d.precision == HB_PREC_EXACT) {
+        cudaError_t e = gaussian_exact_fused(in, zo, nzo, (float*)out, d.taps, epi, tmp, s, launches);
+        if (e != cudaErrorNotSupported) return e;
+        cudaGetLastError();
+      }
       return gaussian_generic(in, zo, nzo, (float*)out, d.taps,
                               d.precision == HB_PREC_EXACT, epi, tmp, s, launches);
     }
@@ -334,7 +339,11 @@ cudaError_t run_stage(const StageDesc& d, const DevIn& in, int64_t zo, int64_t n
           e = gaussian_generic(in, g0, g1 - g0, g, d.taps, false, none, tmp, s, launches);
         }
       } else {
-        e = gaussian_generic(in, g0, g1 - g0, g, d.taps, true, none, tmp, s, launches);
+        e = gaussian_exact_fused(in, g0, g1 - g0, g, d.taps, none, tmp, s, launches);
+        if (e == cudaErrorNotSupported) {
+          cudaGetLastError();
+          e = gaussian_generic(in, g0, g1 - g0, g, d.taps, true, none, tmp, s, launches);
+        }
       }
       if (e != cudaSuccess) return e;
       return log_diff(g, g0, g1 - g0, in.nz, in.ny, in.nx, zo, nzo, (float*)out, s, launches);

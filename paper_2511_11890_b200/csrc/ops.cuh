@@ -65,6 +65,11 @@ cudaError_t gaussian_fused(const DevIn& in, int64_t zo, int64_t nzo, float* out,
                            const Taps& taps, const EpiArgs& epi, cudaStream_t s,
                            int64_t* launches);
 
+// bit-exact Gaussian in two kernels (gauss_exact.cu); tmp: nzo*ny*nx floats
+cudaError_t gaussian_exact_fused(const DevIn& in, int64_t zo, int64_t nzo, float* out,
+                                 const Taps& taps, const EpiArgs& epi, float* tmp,
+                                 cudaStream_t s, int64_t* launches);
+
 cudaError_t mean_fused(const DevIn& in, int64_t zo, int64_t nzo, float* out, int r,
                        cudaStream_t s, int64_t* launches);
 
