@@ -70,9 +70,7 @@ bool make_tmap_3d(CUtensorMap* map, const void* base, CUtensorMapDataType dt, in
 
 namespace {
 
-constexpr int TX = 48, TY = 32, NT = 256;
-constexpr int SY_STRIDE = 80;  // floats; = 16 (mod 32) -> conflict-free LDS.64 in the X pass
-constexpr int SEG = 6;         // outputs per thread along x (48 / 8)
+constexpr int TY = 32, NT = 256;
 
 enum { MODE_GAUSS = 0, MODE_BOX = 1 };
 
@@ -96,6 +94,14 @@ template <> struct TmaType<uint8_t> { static constexpr CUtensorMapDataType v = C
 
 template <int R, typename Tin>
 struct Geo {
+  // Tile width: 48 x 32 with 6 outputs per thread for small radii; 32 x 32 with
+  // 4 outputs per thread for R >= 4 so the 17-deep register ring (68 regs)
+  // leaves room for two CTAs (16 warps) per SM.
+  static constexpr int TX = R >= 4 ? 32 : 48;
+  static constexpr int SEG = TX / 8;                                    // outputs per thread (x)
+  // sY pitch: conflict-free LDS.64 in the X pass (80 = 16 mod 32 for 6-wide
+  // segments; 50 = 2 mod 4 for 4-wide segments)
+  static constexpr int SYS = R >= 4 ? 50 : 80;
   static constexpr int WC = TX + 2 * R;                                 // halo'd width
   static constexpr int HB = TY + 2 * R;                                 // halo'd height
   static constexpr int ALIGN = 16 / (int)sizeof(Tin);                   // 16 B in elements
@@ -108,15 +114,15 @@ struct Geo {
   static constexpr int STAGE_BYTES = HB * WBOX * (int)sizeof(Tin);
   static constexpr int STAGE_PITCH = (STAGE_BYTES + 127) / 128 * 128;
   static constexpr int NST = R <= 1 ? 4 : (R <= 3 ? 6 : 3);            // TMA ring depth
-  static constexpr int MINB = R <= 1 ? 3 : (R <= 3 ? 2 : 1);           // CTAs per SM
+  static constexpr int MINB = R <= 1 ? 3 : 2;                           // CTAs per SM
   static constexpr int RING = 2 * R + 1;
-  static constexpr int SY_BYTES = 2 * TY * SY_STRIDE * 4;
+  static constexpr int SY_BYTES = 2 * TY * SYS * 4;
   static constexpr int SOUT_BYTES = 2 * TY * TX * 4;
   static constexpr int OFF_SY = NST * STAGE_PITCH;
   static constexpr int OFF_SOUT = OFF_SY + SY_BYTES;
   static constexpr int OFF_BAR = OFF_SOUT + SOUT_BYTES;
   static constexpr int SMEM = OFF_BAR + NST * 8 + 128;  // +128 for base alignment
-  static_assert(WC <= SY_STRIDE, "halo'd tile wider than the sY pitch");
+  static_assert(WC <= SYS, "halo'd tile wider than the sY pitch");
 };
 
 template <typename T>
@@ -136,11 +142,11 @@ k_sep3d_fused(const __grid_constant__ CUtensorMap tin, const __grid_constant__ C
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + G::OFF_BAR);
 
   const int tid = threadIdx.x;
-  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
+  const int x0 = blockIdx.x * G::TX, y0 = blockIdx.y * TY;
   const int z0 = blockIdx.z * a.zchunk;
   const int z1 = min(z0 + a.zchunk, a.nzo);
   const int nsl = (z1 - z0) + 2 * R;  // input slices this CTA consumes
-  const bool border = (x0 - R < 0) || (x0 + TX + R > a.nx) || (y0 - R < 0) || (y0 + TY + R > a.ny);
+  const bool border = (x0 - R < 0) || (x0 + G::TX + R > a.nx) || (y0 - R < 0) || (y0 + TY + R > a.ny);
 
   const float* w = a.w;  // taps stay in the constant bank (FFMA c[] operand)
 
@@ -168,13 +174,13 @@ k_sep3d_fused(const __grid_constant__ CUtensorMap tin, const __grid_constant__ C
   // X-pass mapping: warp -> 4 rows, lane -> (row r, 6-wide segment j)
   const int lane = tid & 31, warp = tid >> 5;
   const int xr = 4 * warp + (lane >> 3);  // output row in tile (0..31)
-  const int xj = (lane & 7) * SEG;        // output col start in tile
+  const int xj = (lane & 7) * G::SEG;        // output col start in tile
 
-  float ring[G::RING][SEG];
+  float ring[G::RING][G::SEG];
 #pragma unroll
   for (int u = 0; u < G::RING; ++u)
 #pragma unroll
-    for (int m = 0; m < SEG; ++m) ring[u][m] = 0.f;
+    for (int m = 0; m < G::SEG; ++m) ring[u][m] = 0.f;
 
   for (int s = 0; s < nsl; ++s) {
     const int st = s % G::NST;
@@ -195,7 +201,7 @@ k_sep3d_fused(const __grid_constant__ CUtensorMap tin, const __grid_constant__ C
       __syncthreads();
     }
     // ---- Y pass: sIn -> sY[s&1] -------------------------------------------
-    float* sYb = sY + (s & 1) * TY * SY_STRIDE;
+    float* sYb = sY + (s & 1) * TY * G::SYS;
     if (y_active) {
       float v[8 + 2 * R];
 #pragma unroll
@@ -212,7 +218,7 @@ k_sep3d_fused(const __grid_constant__ CUtensorMap tin, const __grid_constant__ C
 #pragma unroll
           for (int k = 1; k < 2 * R + 1; ++k) acc += v[j + k];
         }
-        sYb[(8 * yg + j) * SY_STRIDE + yc] = acc;
+        sYb[(8 * yg + j) * G::SYS + yc] = acc;
       }
     }
     __syncthreads();
@@ -226,24 +232,24 @@ k_sep3d_fused(const __grid_constant__ CUtensorMap tin, const __grid_constant__ C
       // store the output tile produced in the previous iteration
       const int o_prev = s - 1 - 2 * R;
       if (o_prev >= 0) {
-        tma_store_3d(&tout, sOut + (o_prev & 1) * TY * TX, x0, y0, z0 + o_prev);
+        tma_store_3d(&tout, sOut + (o_prev & 1) * TY * G::TX, x0, y0, z0 + o_prev);
         bulk_commit();
         bulk_wait_read<1>();  // the store before it has finished reading its buffer
       }
     }
     // ---- X pass: sY -> 6 values -------------------------------------------
-    float xo[SEG];
+    float xo[G::SEG];
     {
-      float v[SEG + 2 * R];
-      const float* row = sYb + xr * SY_STRIDE + xj;
+      float v[G::SEG + 2 * R];
+      const float* row = sYb + xr * G::SYS + xj;
 #pragma unroll
-      for (int i = 0; i < (SEG + 2 * R) / 2; ++i) {
+      for (int i = 0; i < (G::SEG + 2 * R) / 2; ++i) {
         const float2 t = *reinterpret_cast<const float2*>(row + 2 * i);
         v[2 * i] = t.x;
         v[2 * i + 1] = t.y;
       }
 #pragma unroll
-      for (int m = 0; m < SEG; ++m) {
+      for (int m = 0; m < G::SEG; ++m) {
         float acc;
         if (MODE == MODE_GAUSS) {
           acc = v[m + R] * w[R];
@@ -259,16 +265,16 @@ k_sep3d_fused(const __grid_constant__ CUtensorMap tin, const __grid_constant__ C
     }
     // ---- ring insert + Z pass ----------------------------------------------
     const int o = s - 2 * R;  // output slice produced now (if >= 0)
-    float zo_[SEG];
+    float zo_[G::SEG];
     bool have = false;
     switch (s % G::RING) {
 #define HB_RING_CASE(U)                                                           \
   case U:                                                                         \
     if constexpr (U < G::RING) {                                                  \
-      _Pragma("unroll") for (int m = 0; m < SEG; ++m) ring[U][m] = xo[m];         \
+      _Pragma("unroll") for (int m = 0; m < G::SEG; ++m) ring[U][m] = xo[m];         \
       if (o >= 0) {                                                               \
         have = true;                                                              \
-        _Pragma("unroll") for (int m = 0; m < SEG; ++m) {                         \
+        _Pragma("unroll") for (int m = 0; m < G::SEG; ++m) {                         \
           float acc;                                                              \
           if (MODE == MODE_GAUSS) {                                               \
             acc = ring[(U + 1 + R) % G::RING][m] * w[R];                          \
@@ -295,22 +301,22 @@ k_sep3d_fused(const __grid_constant__ CUtensorMap tin, const __grid_constant__ C
     if (have) {
       if (MODE == MODE_BOX) {
 #pragma unroll
-        for (int m = 0; m < SEG; ++m) zo_[m] = __fdiv_rn(zo_[m], a.count);
+        for (int m = 0; m < G::SEG; ++m) zo_[m] = __fdiv_rn(zo_[m], a.count);
       }
       if (UNSHARP) {
         const int gy = y0 + xr;
         const int64_t zb = (int64_t)a.zo + z0 + o;
         const Tin* orow = reinterpret_cast<const Tin*>(a.orig) + (zb * a.ny + min(gy, a.ny - 1)) * (int64_t)a.nx;
 #pragma unroll
-        for (int m = 0; m < SEG; ++m) {
+        for (int m = 0; m < G::SEG; ++m) {
           const int gx = min(x0 + xj + m, a.nx - 1);
           const float b = cvt(__ldg(orow + gx));
           zo_[m] = __fadd_rn(b, __fmul_rn(a.amount, __fsub_rn(b, zo_[m])));
         }
       }
-      float* dst = sOut + (o & 1) * TY * TX + xr * TX + xj;
+      float* dst = sOut + (o & 1) * TY * G::TX + xr * G::TX + xj;
 #pragma unroll
-      for (int m = 0; m < SEG; m += 2) *reinterpret_cast<float2*>(dst + m) = make_float2(zo_[m], zo_[m + 1]);
+      for (int m = 0; m < G::SEG; m += 2) *reinterpret_cast<float2*>(dst + m) = make_float2(zo_[m], zo_[m + 1]);
       fence_proxy_async();
     }
   }
@@ -318,7 +324,7 @@ k_sep3d_fused(const __grid_constant__ CUtensorMap tin, const __grid_constant__ C
   if (tid == 0) {
     const int o_last = nsl - 1 - 2 * R;
     if (o_last >= 0) {
-      tma_store_3d(&tout, sOut + (o_last & 1) * TY * TX, x0, y0, z0 + o_last);
+      tma_store_3d(&tout, sOut + (o_last & 1) * TY * G::TX, x0, y0, z0 + o_last);
       bulk_commit();
     }
     bulk_wait<0>();
@@ -332,7 +338,7 @@ cudaError_t launch(const DevIn& in, int64_t zo, int64_t nzo, float* out, const T
   CUtensorMap tin, tout;
   if (!make_tmap_3d(&tin, in.p, TmaType<Tin>::v, sizeof(Tin), in.nx, in.ny, in.nz, G::WBOX, G::HB))
     return cudaErrorNotSupported;
-  if (!make_tmap_3d(&tout, out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, in.nx, in.ny, nzo, TX, TY))
+  if (!make_tmap_3d(&tout, out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, in.nx, in.ny, nzo, G::TX, TY))
     return cudaErrorNotSupported;
   FusedArgs a;
   for (int k = 0; k < 2 * R + 1; ++k) a.w[k] = taps.w[k];
@@ -344,7 +350,7 @@ cudaError_t launch(const DevIn& in, int64_t zo, int64_t nzo, float* out, const T
   a.count = epi.count;
   a.orig = epi.orig;
   a.amount = epi.amount;
-  const int gx = (int)((in.nx + TX - 1) / TX), gy = (int)((in.ny + TY - 1) / TY);
+  const int gx = (int)((in.nx + G::TX - 1) / G::TX), gy = (int)((in.ny + TY - 1) / TY);
   // z-chunking: balance waves of (148 * MINB) resident CTAs against the 2R-slice
   // priming cost of every chunk
   const int64_t tiles = (int64_t)gx * gy;
