@@ -210,17 +210,31 @@ struct Net {
     a = lo;
     cc = hi;
   }
-  // sorted 3x3 neighbourhood: in r[row][col] (row-major), out s[0..8] ascending
-  __device__ __forceinline__ void plane(int (&r)[3][3], int (&s)[9]) const {
-#pragma unroll
-    for (int i = 0; i < 3; ++i) sort3(r[i][0], r[i][1], r[i][2]);  // rows
-#pragma unroll
-    for (int j = 0; j < 3; ++j) sort3(r[0][j], r[1][j], r[2][j]);  // columns
-    // tableau -> sorted, wire order (0,0),(0,1),(1,0),(0,2),(1,1),(2,0),(1,2),(2,1),(2,2)
-    s[0] = r[0][0]; s[1] = r[0][1]; s[2] = r[1][0]; s[3] = r[0][2]; s[4] = r[1][1];
-    s[5] = r[2][0]; s[6] = r[1][2]; s[7] = r[2][1]; s[8] = r[2][2];
+  // 3x3 matrix sorted along both axes (Young tableau) -> ascending s[0..8];
+  // wire order (0,0),(0,1),(1,0),(0,2),(1,1),(2,0),(1,2),(2,1),(2,2) + 7 CE
+  // (tools/netgen: exhaustive over the 20 monotone 0/1 tableaux)
+  __device__ __forceinline__ void tableau(const int (&m)[3][3], int (&s)[9]) const {
+    s[0] = m[0][0]; s[1] = m[0][1]; s[2] = m[1][0]; s[3] = m[0][2]; s[4] = m[1][1];
+    s[5] = m[2][0]; s[6] = m[1][2]; s[7] = m[2][1]; s[8] = m[2][2];
     ce(s[3], s[5]); ce(s[1], s[2]); ce(s[2], s[3]); ce(s[6], s[7]);
     ce(s[5], s[6]); ce(s[3], s[4]); ce(s[4], s[5]);
+  }
+  // the sorted planes of two x-adjacent outputs from r[row][x-1..x+2]: the four
+  // vertical triples are sorted once and shared, then each plane sorts across
+  // its three columns per rank (rows and columns sorted -> tableau)
+  __device__ __forceinline__ void planes2(int (&r)[3][4], int (&pa)[9], int (&pb)[9]) const {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) sort3(r[0][j], r[1][j], r[2][j]);
+    int a[3][3], b[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      a[i][0] = r[i][0]; a[i][1] = r[i][1]; a[i][2] = r[i][2];
+      b[i][0] = r[i][1]; b[i][1] = r[i][2]; b[i][2] = r[i][3];
+      sort3(a[i][0], a[i][1], a[i][2]);
+      sort3(b[i][0], b[i][1], b[i][2]);
+    }
+    tableau(a, pa);
+    tableau(b, pb);
   }
   // ranks 4..13 of cur ∪ nxt (two sorted 9-lists) -> m[0..9]
   __device__ __forceinline__ void merge(const int (&cur)[9], const int (&nxt)[9], int (&m)[10]) const {
@@ -253,7 +267,12 @@ struct Net {
     const int t7 = max(m[2], p[6]);
     const int t8 = max(m[1], p[7]);
     const int t9 = max(m[0], p[8]);
-    return min(min(min(t0, t1), min(t2, t3)), min(min(min(t4, t5), min(t6, t7)), min(t8, t9)));
+    // chained 3-input mins (VIMNMX3): 5 ALU ops instead of 9
+    int r = min(t0, min(t1, t2));
+    r = min(r, min(t3, t4));
+    r = min(r, min(t5, t6));
+    r = min(r, min(t7, t8));
+    return min(r, t9);
   }
 };
 
@@ -264,7 +283,7 @@ template <typename T>
 __global__ void __launch_bounds__(256, 2)
 k_median3_plane(const T* __restrict__ in, int64_t nz, int64_t ny, int64_t nx, int64_t zo,
                 int64_t nzo, int zchunk, T* __restrict__ out, ImadOnes ones) {
-  __shared__ __align__(16) int tile[2][M3_H][M3_W];
+  __shared__ __align__(16) int tile[3][M3_H][M3_W];
   const Net net{ones};
   const int tid = threadIdx.x;
   const int tx = tid & 31, ty = tid >> 5;
@@ -305,16 +324,7 @@ k_median3_plane(const T* __restrict__ in, int64_t nz, int64_t ny, int64_t nx, in
       const int2 hi = *reinterpret_cast<const int2*>(&tile[buf][ty + i][2 * tx + 2]);
       r[i][0] = lo.x; r[i][1] = lo.y; r[i][2] = hi.x; r[i][3] = hi.y;
     }
-    int a[3][3], b[3][3];
-#pragma unroll
-    for (int i = 0; i < 3; ++i)
-#pragma unroll
-      for (int j = 0; j < 3; ++j) {
-        a[i][j] = r[i][j];
-        b[i][j] = r[i][j + 1];
-      }
-    net.plane(a, pa);
-    net.plane(b, pb);
+    net.planes2(r, pa, pb);
   };
   const int64_t gy = y0 + ty, gx = x0 + 2 * tx;
   const bool st_y = gy < ny, st_x0 = gx < nx, st_x1 = gx + 1 < nx;
@@ -330,24 +340,24 @@ k_median3_plane(const T* __restrict__ in, int64_t nz, int64_t ny, int64_t nx, in
   // with M = ranks 4..13 of P(z) ∪ P(z+1).  Four steps cycle the plane names.
   int X[2][9], Y[2][9], Z[2][9], W[2][9], M[2][10];
   int v[PER];
+  // slice zs-1+k lives in tile[k % 3]; a buffer is rewritten three steps after
+  // it was read, so one barrier per step orders all reads before the rewrite
   fetch(zo + zs - 1, v);
   stash(0, v);
   fetch(zo + zs, v);
-  __syncthreads();
-  planes(0, X[0], X[1]);  // P(zs-1)
   stash(1, v);
   fetch(zo + zs + 1, v);
   __syncthreads();
+  planes(0, X[0], X[1]);  // P(zs-1)
   planes(1, Y[0], Y[1]);  // P(zs)
   int64_t z = zs;
-  int tb = 0;  // smem buffer that receives slice z+1
+  int tb = 2;  // buffer of slice z+1
   auto next_plane = [&](int (&pa)[9], int (&pb)[9]) {
-    __syncthreads();  // everyone finished reading buffer tb (slice z-1)
     stash(tb, v);
     fetch(zo + z + 2, v);
     __syncthreads();
     planes(tb, pa, pb);
-    tb ^= 1;
+    tb = tb == 2 ? 0 : tb + 1;
   };
   auto emit2 = [&](int m0, int m1) {
     emit(zo + z, m0, m1);
