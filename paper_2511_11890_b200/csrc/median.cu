@@ -280,7 +280,7 @@ constexpr int M3_TX = 64, M3_TY = 8;  // outputs per CTA slice (32 x-pairs x 8 r
 constexpr int M3_W = M3_TX + 2, M3_H = M3_TY + 2;
 
 template <typename T>
-__global__ void __launch_bounds__(256, 2)
+__global__ void __launch_bounds__(256, 3)
 k_median3_plane(const T* __restrict__ in, int64_t nz, int64_t ny, int64_t nx, int64_t zo,
                 int64_t nzo, int zchunk, T* __restrict__ out, ImadOnes ones) {
   __shared__ __align__(16) int tile[3][M3_H][M3_W];
@@ -303,16 +303,18 @@ k_median3_plane(const T* __restrict__ in, int64_t nz, int64_t ny, int64_t nx, in
     const int64_t gy = clamp64(y0 - 1 + ly, 0, ny - 1), gx = clamp64(x0 - 1 + lx, 0, nx - 1);
     goff[k] = gy * nx + gx;
   }
-  auto fetch = [&](int64_t zb, int (&v)[PER]) {
+  // fetch keeps the raw samples; the key conversion happens in stash, one
+  // step later, so the global-load latency overlaps a whole step of sorting
+  auto fetch = [&](int64_t zb, T (&v)[PER]) {
     const T* src = in + clamp64(zb, 0, nz - 1) * ny * nx;
 #pragma unroll
-    for (int k = 0; k < PER; ++k) v[k] = gval[k] ? to_key<T>(__ldg(src + goff[k])) : 0;
+    for (int k = 0; k < PER; ++k) v[k] = gval[k] ? __ldg(src + goff[k]) : T(0);
   };
-  auto stash = [&](int buf, const int (&v)[PER]) {
+  auto stash = [&](int buf, const T (&v)[PER]) {
 #pragma unroll
     for (int k = 0; k < PER; ++k) {
       const int e = tid + 256 * k;
-      if (gval[k]) (&tile[buf][0][0])[e] = v[k];
+      if (gval[k]) (&tile[buf][0][0])[e] = to_key<T>(v[k]);
     }
   };
   // this thread's two planes of slice `buf`
@@ -339,7 +341,7 @@ k_median3_plane(const T* __restrict__ in, int64_t nz, int64_t ny, int64_t nx, in
   // One merge serves two outputs: out(z) = sel(M, P(z-1)), out(z+1) = sel(M, P(z+2))
   // with M = ranks 4..13 of P(z) ∪ P(z+1).  Four steps cycle the plane names.
   int X[2][9], Y[2][9], Z[2][9], W[2][9], M[2][10];
-  int v[PER];
+  T v[PER];
   // slice zs-1+k lives in tile[k % 3]; a buffer is rewritten three steps after
   // it was read, so one barrier per step orders all reads before the rewrite
   fetch(zo + zs - 1, v);
