@@ -135,14 +135,16 @@ def dist_setup(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # one process per GPU; on a box with fewer GPUs than ranks (functional
+    # testing only) ranks share devices round-robin
+    dev = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(dev)
     if world > 1:
         import torch.distributed as dist
 
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    else:
-        torch.cuda.set_device(local)
-    os.environ["HARPIA_DEVICE"] = str(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+    os.environ["HARPIA_DEVICE"] = str(dev)
+    local = dev
     return world, rank, local
 
 

@@ -107,7 +107,7 @@ k_exact_yx(const __grid_constant__ CUtensorMap tm, float* __restrict__ out, cons
   using G = EGeo<R>;
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem =
-      reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~(uintptr_t)127);
+      smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u)  /* stays in .shared */;
   float* sIn = reinterpret_cast<float*>(smem);
   float* sY = sIn + G::HB * G::WBOX;
   uint64_t* bar = reinterpret_cast<uint64_t*>(sY + EY_TY * G::SY + ((EY_TY * G::SY) & 1));

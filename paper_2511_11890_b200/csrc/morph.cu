@@ -230,7 +230,7 @@ k_morph2(const __grid_constant__ CUtensorMap tin, T* __restrict__ out, const Mor
   constexpr int RING = 2 * EZ + 1;
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem =
-      reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~(uintptr_t)127);
+      smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u)  /* stays in .shared */;
   T* sraw = reinterpret_cast<T*>(smem);
   uint32_t* runs = reinterpret_cast<uint32_t*>(smem + a.off_runs);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + a.off_bar);
@@ -557,7 +557,7 @@ k_morph3(const __grid_constant__ CUtensorMap tin, T* __restrict__ out, const Mor
   constexpr int WPR = M3X_TX / 2;  // u16x2 words per H row (32)
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem =
-      reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~(uintptr_t)127);
+      smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u)  /* stays in .shared */;
   T* sraw = reinterpret_cast<T*>(smem);
   uint32_t* sH = reinterpret_cast<uint32_t*>(smem + M3X_NST * STAGE_PITCH);  // [R][HY][WPR]
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + M3X_NST * STAGE_PITCH + (R > 0 ? R : 1) * HY * WPR * 4);
