@@ -137,15 +137,25 @@ def dist_setup(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     # one process per GPU; on a box with fewer GPUs than ranks (functional
     # testing only) ranks share devices round-robin
-    dev = local % max(1, torch.cuda.device_count())
+    ndev = max(1, torch.cuda.device_count())
+    dev = local % ndev
     torch.cuda.set_device(dev)
+    global _DIST_DEVICE
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        if world <= ndev:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+            _DIST_DEVICE = "cuda"
+        else:  # NCCL refuses two ranks per GPU: plumbing over gloo
+            dist.init_process_group("gloo")
+            _DIST_DEVICE = "cpu"
     os.environ["HARPIA_DEVICE"] = str(dev)
     local = dev
     return world, rank, local
+
+
+_DIST_DEVICE = "cuda"
 
 
 def barrier(world):
@@ -161,7 +171,7 @@ def max_over_ranks(world, value: float) -> float:
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([value], dtype=torch.float64, device="cuda")
+    t = torch.tensor([value], dtype=torch.float64, device=_DIST_DEVICE)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -388,7 +398,7 @@ def extra_breakdown(n, peak):
     res = {}
     stream = torch.cuda.current_stream()
 
-    def timeit(fn, reps=5):
+    def timeit(fn, reps=5):  # device time per call, CUDA events on the launch stream
         fn()
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -409,13 +419,35 @@ def extra_breakdown(n, peak):
             res[f"gaussian_s2_{edge}_{prec}"] = {"gvox_s": round(v / ms / 1e6, 3), "ms": round(ms, 3),
                                                  "hbm_frac": round(8 * v / ms / 1e6 / peak, 4)}
         del x, o
-    u = torch.randint(0, 65535, (n + 6, n, n), device="cuda", dtype=torch.int32).to(torch.uint16)
-    ou = torch.empty((n, n, n), device="cuda", dtype=torch.uint16)
-    prog = morphology.morph_program("erode", morphology.StructuringElement.ball(3))
-    ms = timeit(lambda: _native.apply_device(u, ou, prog, 3, stream))
-    res[f"erode_ball3_u16_{n}"] = {"gvox_s": round(n ** 3 / ms / 1e6, 3), "ms": round(ms, 3),
-                                   "hbm_frac": round(4 * n ** 3 / ms / 1e6 / peak, 4)}
-    del u, ou
+    # configs[2]: grey (u16) and binary (u8) erosion + dilation, ball:3, 2048^3
+    big = 2048
+    ball = morphology.StructuringElement.ball(3)
+    for dtn, tdt in (("u16", torch.uint16), ("u8", torch.uint8)):
+        if dtn == "u16":
+            src = torch.randint(0, 65535, (big + 6, big, big), device="cuda", dtype=torch.int32).to(tdt)
+        else:
+            src = (torch.rand((big + 6, big, big), device="cuda") < 0.5).to(tdt)
+        dst = torch.empty((big, big, big), device="cuda", dtype=tdt)
+        for opn in ("erode", "dilate"):
+            prog = morphology.morph_program(opn, ball)
+            ms = timeit(lambda: _native.apply_device(src, dst, prog, 3, stream), reps=3)
+            nb = 2 * src.element_size()
+            res[f"{opn}_ball3_{dtn}_{big}"] = {"gvox_s": round(big ** 3 / ms / 1e6, 3), "ms": round(ms, 3),
+                                               "hbm_frac": round(nb * big ** 3 / ms / 1e6 / peak, 4)}
+        del src, dst
+        torch.cuda.synchronize()
+    # configs[3] (per-GPU slab, 1024^3): unsharp(sigma=1, a=1.5) -> LoG(sigma=2) fused chain,
+    # and the two stages alone
+    x = torch.rand((n + 28, n, n), device="cuda")
+    o = torch.empty((n, n, n), device="cuda")
+    chain = filters.chain(filters.unsharp_program(1.0, 1.5), filters.log_program(2.0))
+    for name, prog, zb in (("unsharp_s1", filters.unsharp_program(1.0, 1.5), 4),
+                           ("log_s2_exact", filters.log_program(2.0), 10),
+                           ("unsharp_then_log_chain", chain, 14)):
+        ms = timeit(lambda: _native.apply_device(x, o, prog, zb, stream), reps=3)
+        res[f"{name}_{n}"] = {"gvox_s": round(n ** 3 / ms / 1e6, 3), "ms": round(ms, 3),
+                              "hbm_frac": round(8 * n ** 3 / ms / 1e6 / peak, 4)}
+    del x, o
     torch.cuda.synchronize()
     return res
 

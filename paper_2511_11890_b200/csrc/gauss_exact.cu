@@ -98,6 +98,7 @@ struct YXArgs {
   int orig_dt;
   int64_t orig_zo;   // block z of tmp slice 0
   float amount;
+  int zbase;         // first slice of this launch (gridDim.z <= 65535)
 };
 
 template <int R, bool UNSHARP, typename To>
@@ -112,7 +113,7 @@ k_exact_yx(const __grid_constant__ CUtensorMap tm, float* __restrict__ out, cons
   float* sY = sIn + G::HB * G::WBOX;
   uint64_t* bar = reinterpret_cast<uint64_t*>(sY + EY_TY * G::SY + ((EY_TY * G::SY) & 1));
   const int tid = threadIdx.x;
-  const int x0 = blockIdx.x * EY_TX, y0 = blockIdx.y * EY_TY, z = blockIdx.z;
+  const int x0 = blockIdx.x * EY_TX, y0 = blockIdx.y * EY_TY, z = blockIdx.z + b.zbase;
   if (tid == 0) {
     mbar_init(bar, 1);
     fence_mbar_init();
@@ -193,7 +194,9 @@ cudaError_t run_exact_r(const DevIn& in, int64_t zo, int64_t nzo, float* out, co
   // Z pass -> tmp (nzo slices)
   {
     const int64_t cols = (plane + EZ_T - 1) / EZ_T;
-    int64_t want = std::max<int64_t>(1, (8 * kNumSMs + cols - 1) / cols);
+    // enough column-chunks in flight to hide the per-step load latency (the
+    // window priming costs 2R extra L2 reads per chunk)
+    int64_t want = std::max<int64_t>((nzo + 127) / 128, (32 * kNumSMs + cols - 1) / cols);
     int zchunk = (int)std::max<int64_t>(std::min<int64_t>(nzo, 4 * R + 8), (nzo + want - 1) / want);
     dim3 grid((unsigned)cols, (unsigned)((nzo + zchunk - 1) / zchunk));
     k_exact_z<R, T><<<grid, EZ_T, 0, s>>>((const T*)in.p, in.nz, plane, zo, nzo, zchunk, tmp, a);
@@ -212,16 +215,19 @@ cudaError_t run_exact_r(const DevIn& in, int64_t zo, int64_t nzo, float* out, co
   b.orig_dt = epi.orig_dt;
   b.orig_zo = epi.orig_zo;
   b.amount = epi.amount;
-  dim3 grid((unsigned)((in.nx + EY_TX - 1) / EY_TX), (unsigned)((in.ny + EY_TY - 1) / EY_TY),
-            (unsigned)nzo);
-  if (epi.kind == EPI_UNSHARP) {
-    auto k = k_exact_yx<R, true, T>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
-    k<<<grid, EY_NT, G::SMEM, s>>>(tm, out, a, b);
-  } else {
-    auto k = k_exact_yx<R, false, T>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
-    k<<<grid, EY_NT, G::SMEM, s>>>(tm, out, a, b);
+  for (int64_t zb = 0; zb < nzo; zb += 65535) {
+    b.zbase = (int)zb;
+    dim3 grid((unsigned)((in.nx + EY_TX - 1) / EY_TX), (unsigned)((in.ny + EY_TY - 1) / EY_TY),
+              (unsigned)std::min<int64_t>(65535, nzo - zb));
+    if (epi.kind == EPI_UNSHARP) {
+      auto k = k_exact_yx<R, true, T>;
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
+      k<<<grid, EY_NT, G::SMEM, s>>>(tm, out, a, b);
+    } else {
+      auto k = k_exact_yx<R, false, T>;
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
+      k<<<grid, EY_NT, G::SMEM, s>>>(tm, out, a, b);
+    }
   }
   if (launches) *launches += 1;
   return cudaGetLastError();

@@ -7,6 +7,8 @@
 // with separately rounded f64 multiply and add (no FMA contraction), then a
 // float32 round per pass.  The fused fast kernel (gauss_fused.cu) is the
 // throughput path; this file is its fallback and the LoG smoothing stage.
+#include <algorithm>
+
 #include "ops.cuh"
 
 namespace hb {
@@ -133,47 +135,89 @@ cudaError_t dispatch_dt(const DevIn& in, int64_t zo, int64_t nzo, float* out,
 // ---- LoG second stage ------------------------------------------------------
 // cd(f)[i] = 0.5f * (f[clamp(i+1)] - f[clamp(i-1)])   (filters.py:234-243)
 // second(i) = 0.5f * (cd[clamp(i+1)] - cd[clamp(i-1)])
-__device__ __forceinline__ float gat(const float* g, int64_t gz0, int64_t plane, int64_t nx,
-                                     int64_t z, int64_t y, int64_t x) {
-  return __ldg(g + (z - gz0) * plane + y * nx + x);
-}
 
-__global__ void __launch_bounds__(kThreads)
-k_log_diff(const float* __restrict__ g, int64_t gz0, int64_t nz, int64_t ny, int64_t nx,
-           int64_t zo, int64_t nzo, float* __restrict__ out) {
-  const int64_t plane = ny * nx;
-  const int64_t total = nzo * plane;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    int64_t zl = i / plane;
-    int64_t r = i - zl * plane;
-    int64_t y = r / nx;
-    int64_t x = r - y * nx;
-    int64_t z = zl + zo;
-    float second[3];
+// One CTA = 32 x 8 (x, y) tile marching down a z-chunk.  Each slice's tile
+// plus a 2-voxel x/y halo is staged in smem (cooperative, prefetched one slice
+// ahead in registers), so xx and yy come from smem; zz comes from a 5-slice
+// register window per thread.  32-bit in-plane math.
+constexpr int LD_TX = 32, LD_TY = 8, LD_W = LD_TX + 4, LD_H = LD_TY + 4;
+constexpr int LD_PER = (LD_W * LD_H + 255) / 256;
+
+__global__ void __launch_bounds__(256)
+k_log_diff(const float* __restrict__ g, int64_t gz0, int nz, int ny, int nx, int64_t zo,
+           int nzo, int zchunk, float* __restrict__ out) {
+  __shared__ float tile[2][LD_H][LD_W];
+  const int tid = threadIdx.x;
+  const int x0 = blockIdx.x * LD_TX, y0 = blockIdx.y * LD_TY;
+  const int x = x0 + (tid & 31), y = y0 + (tid >> 5);
+  const int zs = blockIdx.z * zchunk, ze = min(zs + zchunk, nzo);
+  const int64_t plane = (int64_t)ny * nx;
+  // loader: element e -> clamped (gy, gx) offset in a slice
+  int off[LD_PER];
+  bool val[LD_PER];
 #pragma unroll
-    for (int ax = 0; ax < 3; ++ax) {
-      int64_t len = ax == 0 ? nx : (ax == 1 ? ny : nz);
-      int64_t c = ax == 0 ? x : (ax == 1 ? y : z);
-      float d[2];
+  for (int k = 0; k < LD_PER; ++k) {
+    const int e = tid + 256 * k;
+    val[k] = e < LD_W * LD_H;
+    const int ly = val[k] ? e / LD_W : 0, lx = val[k] ? e % LD_W : 0;
+    off[k] = min(max(y0 - 2 + ly, 0), ny - 1) * nx + min(max(x0 - 2 + lx, 0), nx - 1);
+  }
+  auto fetch = [&](int64_t zb, float (&v)[LD_PER]) {
+    const float* src = g + (zb - gz0) * plane;
 #pragma unroll
-      for (int side = 0; side < 2; ++side) {
-        int64_t j = clamp64(side ? c + 1 : c - 1, 0, len - 1);
-        int64_t hi = clamp64(j + 1, 0, len - 1), lo = clamp64(j - 1, 0, len - 1);
-        float fh, fl;
-        if (ax == 0) {
-          fh = gat(g, gz0, plane, nx, z, y, hi); fl = gat(g, gz0, plane, nx, z, y, lo);
-        } else if (ax == 1) {
-          fh = gat(g, gz0, plane, nx, z, hi, x); fl = gat(g, gz0, plane, nx, z, lo, x);
-        } else {
-          fh = gat(g, gz0, plane, nx, hi, y, x); fl = gat(g, gz0, plane, nx, lo, y, x);
-        }
-        d[side] = __fmul_rn(0.5f, __fsub_rn(fh, fl));
+    for (int k = 0; k < LD_PER; ++k) v[k] = val[k] ? __ldg(src + off[k]) : 0.f;
+  };
+  const bool inside = x < nx && y < ny;
+  const float* col = g + (int64_t)min(y, ny - 1) * nx + min(x, nx - 1);
+  auto at = [&](int64_t zz) { return __ldg(col + (zz - gz0) * plane); };
+  // clamped-index second difference over a window held by accessor f
+  auto second = [&](int c, int len, auto f) {
+    const int jp = min(c + 1, len - 1), jm = max(c - 1, 0);
+    const float dp = __fmul_rn(0.5f, __fsub_rn(f(min(jp + 1, len - 1)), f(max(jp - 1, 0))));
+    const float dm = __fmul_rn(0.5f, __fsub_rn(f(min(jm + 1, len - 1)), f(max(jm - 1, 0))));
+    return __fmul_rn(0.5f, __fsub_rn(dp, dm));
+  };
+  float w[5];
+  const int64_t zb0 = zo + zs;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) w[k] = at(min(max(zb0 - 2 + k, (int64_t)0), (int64_t)nz - 1));
+  float v[LD_PER];
+  fetch(zb0, v);
+  int buf = 0;
+  for (int zl = zs; zl < ze; ++zl) {
+    const int64_t z = zo + zl;
+#pragma unroll
+    for (int k = 0; k < LD_PER; ++k)
+      if (val[k]) (&tile[buf][0][0])[tid + 256 * k] = v[k];
+    if (zl + 1 < ze) fetch(z + 1, v);
+    w[4] = at(min(z + 2, (int64_t)nz - 1));
+    __syncthreads();
+    if (inside) {
+      const int zi = (int)z;
+      const int tx = (tid & 31) + 2, ty = (tid >> 5) + 2;
+      float xx, yy, zz;
+      if (x >= 2 && x < nx - 2 && y >= 2 && y < ny - 2 && zi >= 2 && zi < nz - 2) {
+        // interior: no clamp can trigger -> straight-line, same rounding order
+        const float c = tile[buf][ty][tx];
+        auto sec = [](float lo2, float ctr, float hi2) {
+          const float dp = __fmul_rn(0.5f, __fsub_rn(hi2, ctr));
+          const float dm = __fmul_rn(0.5f, __fsub_rn(ctr, lo2));
+          return __fmul_rn(0.5f, __fsub_rn(dp, dm));
+        };
+        xx = sec(tile[buf][ty][tx - 2], c, tile[buf][ty][tx + 2]);
+        yy = sec(tile[buf][ty - 2][tx], c, tile[buf][ty + 2][tx]);
+        zz = sec(w[0], w[2], w[4]);
+      } else {
+        auto wz = [&](int i) { return w[i - zi + 2]; };
+        zz = second(zi, nz, wz);
+        xx = second(x, nx, [&](int i) { return tile[buf][ty][tx + (i - x)]; });
+        yy = second(y, ny, [&](int i) { return tile[buf][ty + (i - y)][tx]; });
       }
-      second[ax] = __fmul_rn(0.5f, __fsub_rn(d[1], d[0]));
+      out[(int64_t)zl * plane + (int64_t)y * nx + x] = __fadd_rn(__fadd_rn(xx, yy), zz);
     }
-    // LoG := (xx + yy) + zz
-    out[i] = __fadd_rn(__fadd_rn(second[0], second[1]), second[2]);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) w[k] = w[k + 1];
+    buf ^= 1;
   }
 }
 
@@ -212,8 +256,14 @@ cudaError_t log_diff(const float* g, int64_t gz0, int64_t ngz, int64_t nz, int64
                      int64_t* launches) {
   (void)ngz;
   if (nzo <= 0) return cudaSuccess;
-  int64_t n = nzo * ny * nx;
-  k_log_diff<<<grid_for(n), kThreads, 0, s>>>(g, gz0, nz, ny, nx, zo, nzo, out);
+  const int64_t tiles = ((nx + LD_TX - 1) / LD_TX) * ((ny + LD_TY - 1) / LD_TY);
+  // short z-chunks: each step's loads are latency-bound, so parallelism (many
+  // resident CTAs) hides them; 32 slices keep the window priming cost at ~12%
+  const int64_t want = std::max<int64_t>((nzo + 31) / 32, (64 * kNumSMs + tiles - 1) / tiles);
+  const int zchunk = (int)std::max<int64_t>(8, (nzo + want - 1) / want);
+  dim3 grid((unsigned)((nx + LD_TX - 1) / LD_TX), (unsigned)((ny + LD_TY - 1) / LD_TY),
+            (unsigned)((nzo + zchunk - 1) / zchunk));
+  k_log_diff<<<grid, 256, 0, s>>>(g, gz0, (int)nz, (int)ny, (int)nx, zo, (int)nzo, zchunk, out);
   if (launches) *launches += 1;
   return cudaGetLastError();
 }

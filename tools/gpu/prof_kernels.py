@@ -17,6 +17,8 @@ for _ in range(2):
         _native.apply_device(x, o, filters.mean_program(1), 1, s)
     if 'gauss' in which:
         _native.apply_device(x, o, filters.gaussian_program(2.0), 8, s)
+    if 'log' in which:
+        _native.apply_device(x, o[: n - 4], filters.log_program(2.0), 12, s)
     if 'erode' in which:
         _native.apply_device(u, ou, morphology.morph_program('erode', morphology.StructuringElement.ball(3)), 3, s)
 torch.cuda.synchronize()
