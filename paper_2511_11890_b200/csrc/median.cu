@@ -403,8 +403,19 @@ cudaError_t run_median(const DevIn& in, int64_t zo, int64_t nzo, void* out, int 
   if (r == 1) {
     dim3 grid((unsigned)((in.nx + M3_TX - 1) / M3_TX), (unsigned)((in.ny + M3_TY - 1) / M3_TY), 1);
     const int64_t tiles = (int64_t)grid.x * grid.y;
-    const int64_t want = std::max<int64_t>(1, (8 * kNumSMs + tiles - 1) / tiles);
-    const int zchunk = (int)std::max<int64_t>(16, (nzo + want - 1) / want);
+    // z-chunk: enough CTAs that the wave tail is small (3 CTAs/SM resident),
+    // long enough that the 2-plane prologue per chunk stays ~1%
+    const int64_t slots = 3 * kNumSMs;
+    int zchunk = (int)std::min<int64_t>(nzo, 16);
+    double best = 1e300;
+    for (int64_t zc = std::max<int64_t>(16, nzo / 64); zc <= std::max<int64_t>(16, nzo); zc += 16) {
+      const int64_t ctas = tiles * ((nzo + zc - 1) / zc);
+      const double cost = (double)((ctas + slots - 1) / slots) * (double)(zc + 2);
+      if (cost < best * 0.995) {
+        best = cost;
+        zchunk = (int)zc;
+      }
+    }
     grid.z = (unsigned)((nzo + zchunk - 1) / zchunk);
     k_median3_plane<T><<<grid, 256, 0, s>>>(src, in.nz, in.ny, in.nx, zo, nzo, zchunk, dst,
                                             ImadOnes{1, -1});
