@@ -299,7 +299,7 @@ def run_host(data: np.ndarray, out: np.ndarray, program: DeviceProgram,
     ex.pipeline_depth = int(pipeline_depth)
     ex.device_budget = int(device_budget)
     ex.fault_chunk = int(fault_chunk)
-    ex.host_threads = int(host_threads)
+    ex.host_threads = int(host_threads or os.environ.get("HARPIA_HOST_THREADS", "0"))
     ex.chunk_seconds = ctypes.cast(secs, ctypes.POINTER(ctypes.c_double))
     cb = None
     if cancel is not None:
@@ -368,3 +368,36 @@ def trim_device(dev: Optional[int] = None) -> None:
 
 def device_pool_bytes(dev: Optional[int] = None) -> int:
     return int(load().hb_device_pool_bytes(current_device() if dev is None else int(dev)))
+
+
+class pinned:
+    """Context manager that page-locks numpy arrays (cudaHostRegister) so
+    ``run_operator`` DMAs them directly instead of staging through the pinned
+    ring.  Registration costs ~0.2 s/GiB on the B200 box, so it pays off when
+    the same arrays feed several jobs::
+
+        with pinned(volume, out):
+            for name, p in steps:
+                registry.run_operator(volume, name, p, budget, out=out)
+    """
+
+    def __init__(self, *arrays):
+        self.arrays = [a for a in arrays if a is not None]
+        self._done = []
+
+    def __enter__(self):
+        L = load()
+        for a in self.arrays:
+            if not a.flags.c_contiguous:
+                raise ParameterError("only C-contiguous arrays can be pinned")
+            rc = L.hb_pin(a.ctypes.data, a.nbytes)
+            raise_for_status(rc, last_error())
+            self._done.append(a)
+        return self
+
+    def __exit__(self, *exc):
+        L = load()
+        for a in self._done:
+            L.hb_unpin(a.ctypes.data)
+        self._done.clear()
+        return False

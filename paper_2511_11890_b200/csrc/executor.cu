@@ -491,8 +491,8 @@ cudaError_t d2h_staged(PinnedRing& ring, void* dst, const void* src, size_t byte
 
 int auto_threads(int req) {
   if (req > 0) return req;
-  unsigned n = std::thread::hardware_concurrency();
-  return (int)std::max(1u, std::min(8u, n ? n / 2 : 1u));
+  unsigned n = std::thread::hardware_concurrency();  // measured best: all cores, <= 16
+  return (int)std::max(1u, std::min(16u, n ? n : 1u));
 }
 
 double now_ms() {

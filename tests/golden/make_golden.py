@@ -122,10 +122,20 @@ def main():
     weights = {str(s): F._gaussian_kernel(s).tolist() for s in (0.3, 0.5, 1.0, 1.2, 1.5, 2.0, 2.5, 3.3, 4.0)}
     balls = {str(r): len(M.StructuringElement.ball(r).offsets) for r in (1, 2, 3, 4)}
 
+    # .vol sidecar text (volume.py:28-75)
+    V = ref.volume
+    sidecars = []
+    for dt, shape, spacing, desc in [("float32", (3, 4, 5), (1.0, 0.5, 0.25), "scan A"),
+                                     ("uint16", (64, 2052, 2052), (2.0, 1.0, 1.0), ""),
+                                     ("uint8", (1, 1, 1), (0.1, 0.2, 0.3), "tiny: x")]:
+        m = V.VolumeMeta(dtype=dt, shape=shape, spacing=spacing, description=desc)
+        sidecars.append({"dtype": dt, "shape": list(shape), "spacing": list(spacing),
+                         "description": desc, "text": m.to_text()})
+
     np.savez_compressed(HERE / "golden_arrays.npz", **arrays)
     meta = {"generator": "tests/golden/make_golden.py", "reference": args.ref,
             "cases": cases, "plans": plans, "profiles": profiles, "weights": weights,
-            "ball_sizes": balls}
+            "ball_sizes": balls, "sidecars": sidecars}
     (HERE / "golden_meta.json").write_text(json.dumps(meta, indent=1))
     print(f"{len(cases)} cases, {sum(a.nbytes for a in arrays.values())} bytes raw")
 
