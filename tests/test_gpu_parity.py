@@ -267,3 +267,16 @@ def test_factory_se_fast_path(hb, oracle, dt):
                 s = morphology.StructuringElement.parse(f"{kind}:{r}")
                 assert np.array_equal(morphology.erode(x, s), oracle.erode(x, s.offsets)), (shape, kind, r)
                 assert np.array_equal(morphology.dilate(x, s), oracle.dilate(x, s.offsets)), (shape, kind, r)
+
+
+def test_pinned_context_direct_dma(hb):
+    from paper_2511_11890_b200 import pinned, registry
+    from paper_2511_11890_b200.chunking import MemoryBudget
+
+    x = np.random.default_rng(8).random((64, 96, 128), dtype=np.float32)
+    out = np.empty_like(x)
+    b = MemoryBudget(20 * 96 * 128 * 4 * 4, 1.0)
+    want, _ = registry.run_operator(x, "median", {"radius": 1}, b)
+    with pinned(x, out):
+        got, rep = registry.run_operator(x, "median", {"radius": 1}, b, out=out)
+    assert got is out and np.array_equal(out, want) and rep.device_residual_bytes == 0
