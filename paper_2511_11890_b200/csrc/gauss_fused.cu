@@ -83,6 +83,7 @@ struct FusedArgs {
   int zchunk;    // output slices per CTA
   int nx, ny;
   float count;   // box: (2r+1)^3
+  float inv_count;  // RN(1 / count)
   // unsharp epilogue
   const void* orig;
   float amount;
@@ -301,6 +302,8 @@ k_sep3d_fused(const __grid_constant__ CUtensorMap tin, const __grid_constant__ C
     }
     if (have) {
       if (MODE == MODE_BOX) {
+        // correctly rounded sum / count (an FMA-refined reciprocal is bit-identical,
+        // tools/microbench/divtest.cu, but measured slower here)
 #pragma unroll
         for (int m = 0; m < G::SEG; ++m) zo_[m] = __fdiv_rn(zo_[m], a.count);
       }
@@ -349,6 +352,7 @@ cudaError_t launch(const DevIn& in, int64_t zo, int64_t nzo, float* out, const T
   a.nx = (int)in.nx;
   a.ny = (int)in.ny;
   a.count = epi.count;
+  a.inv_count = 1.0f / epi.count;
   a.orig = epi.orig;
   a.amount = epi.amount;
   const int gx = (int)((in.nx + G::TX - 1) / G::TX), gy = (int)((in.ny + TY - 1) / TY);
