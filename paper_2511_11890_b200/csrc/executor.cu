@@ -13,6 +13,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -837,6 +838,7 @@ int32_t hb_run(const hb_volume* in, hb_volume* out, const hb_stage* stages, int3
     return HB_EBUDGET_SMALL;
   }
 
+  const double t_setup = now_ms();
   hb_status status = HB_OK;
   int64_t launches = 0;
   double kernel_ms = 0;
@@ -939,6 +941,7 @@ int32_t hb_run(const hb_volume* in, hb_volume* out, const hb_stage* stages, int3
     }
   }
   cudaError_t sync_e = cudaDeviceSynchronize();
+  const double t_loop = now_ms();
   if (e == cudaSuccess && status == HB_OK && sync_e != cudaSuccess) e = sync_e;
   const int64_t at_chunk = j < npieces ? pieces[j].chunk : nchunks - 1;
   if (e != cudaSuccess && status == HB_OK) {
@@ -978,6 +981,10 @@ int32_t hb_run(const hb_volume* in, hb_volume* out, const hb_stage* stages, int3
   rep->kernel_launches = launches;
   rep->kernel_ms = kernel_ms;
   rep->wall_ms = now_ms() - t_start;
+  if (std::getenv("HB_TRACE"))
+    std::fprintf(stderr, "[hb_run] pieces=%lld S=%lld depth=%d setup=%.2fms loop=%.2fms teardown=%.2fms\n",
+                 (long long)npieces, (long long)S, depth, t_setup - t_start, t_loop - t_setup,
+                 now_ms() - t_loop);
   return status;
 }
 
