@@ -119,7 +119,10 @@ struct Geo {
   static constexpr int MINB = R <= 1 ? 3 : 2;                           // CTAs per SM
   static constexpr int RING = 2 * R + 1;
   static constexpr int SY_BYTES = 2 * TY * SYS * 4;
-  static constexpr int SOUT_BYTES = 2 * TY * TX * 4;
+  // triple-buffered output tile: the store of output o-3 is known complete
+  // (thread 0's wait_group.read<1> in iteration o-1 precedes this iteration's
+  // barrier), so all threads may overwrite its buffer without racing the TMA
+  static constexpr int SOUT_BYTES = 3 * TY * TX * 4;
   static constexpr int OFF_SY = NST * STAGE_PITCH;
   static constexpr int OFF_SOUT = OFF_SY + SY_BYTES;
   static constexpr int OFF_BAR = OFF_SOUT + SOUT_BYTES;
@@ -234,7 +237,7 @@ k_sep3d_fused(const __grid_constant__ CUtensorMap tin, const __grid_constant__ C
       // store the output tile produced in the previous iteration
       const int o_prev = s - 1 - 2 * R;
       if (o_prev >= 0) {
-        tma_store_3d(&tout, sOut + (o_prev & 1) * TY * G::TX, x0, y0, z0 + o_prev);
+        tma_store_3d(&tout, sOut + (o_prev % 3) * TY * G::TX, x0, y0, z0 + o_prev);
         bulk_commit();
         bulk_wait_read<1>();  // the store before it has finished reading its buffer
       }
@@ -318,7 +321,7 @@ k_sep3d_fused(const __grid_constant__ CUtensorMap tin, const __grid_constant__ C
           zo_[m] = __fadd_rn(b, __fmul_rn(a.amount, __fsub_rn(b, zo_[m])));
         }
       }
-      float* dst = sOut + (o & 1) * TY * G::TX + xr * G::TX + xj;
+      float* dst = sOut + (o % 3) * TY * G::TX + xr * G::TX + xj;
 #pragma unroll
       for (int m = 0; m < G::SEG; m += 2) *reinterpret_cast<float2*>(dst + m) = make_float2(zo_[m], zo_[m + 1]);
       fence_proxy_async();
@@ -328,7 +331,7 @@ k_sep3d_fused(const __grid_constant__ CUtensorMap tin, const __grid_constant__ C
   if (tid == 0) {
     const int o_last = nsl - 1 - 2 * R;
     if (o_last >= 0) {
-      tma_store_3d(&tout, sOut + (o_last & 1) * TY * G::TX, x0, y0, z0 + o_last);
+      tma_store_3d(&tout, sOut + (o_last % 3) * TY * G::TX, x0, y0, z0 + o_last);
       bulk_commit();
     }
     bulk_wait<0>();
@@ -478,7 +481,7 @@ struct GeoX2 {
   static constexpr int RING = 2 * R + 1;
   static constexpr int P2 = NYC + 2;  // sY2 row-pair pitch in float2 (even)
   static constexpr int SY_BYTES = 2 * (X2_TY / 2) * P2 * 8;
-  static constexpr int SOUT_BYTES = 2 * X2_TY * X2_TX * 4;
+  static constexpr int SOUT_BYTES = 3 * X2_TY * X2_TX * 4;  // triple-buffered (see Geo)
   static constexpr int OFF_SY = NST * STAGE_PITCH;
   static constexpr int OFF_SOUT = OFF_SY + SY_BYTES;
   static constexpr int OFF_BAR = OFF_SOUT + SOUT_BYTES;
@@ -582,7 +585,7 @@ k_gauss_x2(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUte
       }
       const int o_prev = s - 1 - 2 * R;
       if (o_prev >= 0) {
-        tma_store_3d(&tout, sOut + (o_prev & 1) * X2_TY * X2_TX, x0, y0, z0 + o_prev);
+        tma_store_3d(&tout, sOut + (o_prev % 3) * X2_TY * X2_TX, x0, y0, z0 + o_prev);
         bulk_commit();
         bulk_wait_read<1>();
       }
@@ -656,7 +659,7 @@ k_gauss_x2(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUte
           }
         }
       }
-      float* dst = sOut + (o & 1) * X2_TY * X2_TX + (2 * yp) * X2_TX + 2 * sg;
+      float* dst = sOut + (o % 3) * X2_TY * X2_TX + (2 * yp) * X2_TX + 2 * sg;
       *reinterpret_cast<float2*>(dst) = make_float2(r0[0], r0[1]);
       *reinterpret_cast<float2*>(dst + X2_TX) = make_float2(r1[0], r1[1]);
       fence_proxy_async();
@@ -666,7 +669,7 @@ k_gauss_x2(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUte
   if (tid == 0) {
     const int o_last = nsl - 1 - 2 * R;
     if (o_last >= 0) {
-      tma_store_3d(&tout, sOut + (o_last & 1) * X2_TY * X2_TX, x0, y0, z0 + o_last);
+      tma_store_3d(&tout, sOut + (o_last % 3) * X2_TY * X2_TX, x0, y0, z0 + o_last);
       bulk_commit();
     }
     bulk_wait<0>();
