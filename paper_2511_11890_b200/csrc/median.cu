@@ -293,7 +293,7 @@ k_median3_plane(const T* __restrict__ in, int64_t nz, int64_t ny, int64_t nx, in
   // cooperative slice loader: element e of the halo'd tile -> (ly, lx)
   constexpr int NE = M3_H * M3_W;
   constexpr int PER = (NE + 255) / 256;
-  int64_t goff[PER];
+  int goff[PER];  // in-plane offsets (a plane has < 2^31 voxels)
   bool gval[PER];
 #pragma unroll
   for (int k = 0; k < PER; ++k) {
@@ -301,41 +301,42 @@ k_median3_plane(const T* __restrict__ in, int64_t nz, int64_t ny, int64_t nx, in
     gval[k] = e < NE;
     const int ly = gval[k] ? e / M3_W : 0, lx = gval[k] ? e % M3_W : 0;
     const int64_t gy = clamp64(y0 - 1 + ly, 0, ny - 1), gx = clamp64(x0 - 1 + lx, 0, nx - 1);
-    goff[k] = gy * nx + gx;
+    goff[k] = (int)(gy * nx + gx);
   }
+  const int64_t plane = ny * nx;
   // fetch keeps the raw samples; the key conversion happens in stash, one
-  // step later, so the global-load latency overlaps a whole step of sorting
-  auto fetch = [&](int64_t zb, T (&v)[PER]) {
-    const T* src = in + clamp64(zb, 0, nz - 1) * ny * nx;
+  // step later, so the global-load latency overlaps a whole step of sorting.
+  // Slices are addressed by a running pointer (clamped only at the volume faces).
+  auto slice_ptr = [&](int64_t zb) { return in + clamp64(zb, 0, nz - 1) * plane; };
+  auto fetch = [&](const T* src, T (&v)[PER]) {
 #pragma unroll
     for (int k = 0; k < PER; ++k) v[k] = gval[k] ? __ldg(src + goff[k]) : T(0);
   };
-  auto stash = [&](int buf, const T (&v)[PER]) {
+  auto stash = [&](int* buf, const T (&v)[PER]) {
 #pragma unroll
-    for (int k = 0; k < PER; ++k) {
-      const int e = tid + 256 * k;
-      if (gval[k]) (&tile[buf][0][0])[e] = to_key<T>(v[k]);
-    }
+    for (int k = 0; k < PER; ++k)
+      if (gval[k]) buf[tid + 256 * k] = to_key<T>(v[k]);
   };
-  // this thread's two planes of slice `buf`
-  auto planes = [&](int buf, int (&pa)[9], int (&pb)[9]) {
+  // this thread's two planes of a tile buffer
+  auto planes = [&](const int* buf, int (&pa)[9], int (&pb)[9]) {
     int r[3][4];
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
-      const int2 lo = *reinterpret_cast<const int2*>(&tile[buf][ty + i][2 * tx]);
-      const int2 hi = *reinterpret_cast<const int2*>(&tile[buf][ty + i][2 * tx + 2]);
+      const int2 lo = *reinterpret_cast<const int2*>(buf + (ty + i) * M3_W + 2 * tx);
+      const int2 hi = *reinterpret_cast<const int2*>(buf + (ty + i) * M3_W + 2 * tx + 2);
       r[i][0] = lo.x; r[i][1] = lo.y; r[i][2] = hi.x; r[i][3] = hi.y;
     }
     net.planes2(r, pa, pb);
   };
   const int64_t gy = y0 + ty, gx = x0 + 2 * tx;
   const bool st_y = gy < ny, st_x0 = gx < nx, st_x1 = gx + 1 < nx;
-  T* orow = out + gy * nx + gx;
-  auto emit = [&](int64_t z, int k0, int k1) {
-    if (!st_y) return;
-    T* o = orow + (z - zo) * ny * nx;
-    if (st_x0) o[0] = from_key<T>(k0);
-    if (st_x1) o[1] = from_key<T>(k1);
+  T* optr = out + (zs) * plane + gy * nx + gx;  // output slice zs, advanced per step
+  auto emit = [&](int k0, int k1) {
+    if (st_y) {
+      if (st_x0) optr[0] = from_key<T>(k0);
+      if (st_x1) optr[1] = from_key<T>(k1);
+    }
+    optr += plane;
   };
 
   // One merge serves two outputs: out(z) = sel(M, P(z-1)), out(z+1) = sel(M, P(z+2))
@@ -344,25 +345,30 @@ k_median3_plane(const T* __restrict__ in, int64_t nz, int64_t ny, int64_t nx, in
   T v[PER];
   // slice zs-1+k lives in tile[k % 3]; a buffer is rewritten three steps after
   // it was read, so one barrier per step orders all reads before the rewrite
-  fetch(zo + zs - 1, v);
-  stash(0, v);
-  fetch(zo + zs, v);
-  stash(1, v);
-  fetch(zo + zs + 1, v);
+  int* const tb0 = &tile[0][0][0];
+  constexpr int TPITCH = M3_H * M3_W;
+  fetch(slice_ptr(zo + zs - 1), v);
+  stash(tb0, v);
+  fetch(slice_ptr(zo + zs), v);
+  stash(tb0 + TPITCH, v);
+  // next slice to fetch: block z = zo + zs + 1, then + 1 per step (clamped at faces)
+  int64_t zf = zo + zs + 1;
+  fetch(slice_ptr(zf), v);
   __syncthreads();
-  planes(0, X[0], X[1]);  // P(zs-1)
-  planes(1, Y[0], Y[1]);  // P(zs)
+  planes(tb0, X[0], X[1]);           // P(zs-1)
+  planes(tb0 + TPITCH, Y[0], Y[1]);  // P(zs)
   int64_t z = zs;
-  int tb = 2;  // buffer of slice z+1
+  int* tb = tb0 + 2 * TPITCH;  // buffer that receives slice z+1
   auto next_plane = [&](int (&pa)[9], int (&pb)[9]) {
     stash(tb, v);
-    fetch(zo + z + 2, v);
+    ++zf;
+    fetch(slice_ptr(zf), v);
     __syncthreads();
     planes(tb, pa, pb);
-    tb = tb == 2 ? 0 : tb + 1;
+    tb = (tb == tb0 + 2 * TPITCH) ? tb0 : tb + TPITCH;
   };
   auto emit2 = [&](int m0, int m1) {
-    emit(zo + z, m0, m1);
+    emit(m0, m1);
     ++z;
   };
   while (z < ze) {
