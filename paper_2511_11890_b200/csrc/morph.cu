@@ -620,7 +620,16 @@ k_morph3(const __grid_constant__ CUtensorMap tin, T* __restrict__ out, const Mor
         const T* row = stage + r * WBOX;
         uint32_t w[6];  // pairs 2q-2 .. 2q+3
 #pragma unroll
-        for (int i = 0; i < 6; ++i) w[i] = word(row, 2 * q - 2 + i);
+        for (int i = 0; i < 6; ++i) {
+          if constexpr (sizeof(T) == 2) {
+            w[i] = word(row, 2 * q - 2 + i);
+          } else {
+            // u8: three aligned 32-bit loads cover voxels 4q-4 .. 4q+7; each
+            // byte pair is widened into u16 lanes with one PRMT
+            const uint32_t b4 = *reinterpret_cast<const uint32_t*>(row + XA2 + 4 * q - 4 + 4 * (i >> 1));
+            w[i] = prmt(b4, 0u, (i & 1) ? 0x4342u : 0x4140u);
+          }
+        }
 #pragma unroll
         for (int j = 0; j < 2; ++j) {  // pair 2q + j -> w[2 + j]
           const uint32_t c = w[2 + j];
@@ -655,7 +664,14 @@ k_morph3(const __grid_constant__ CUtensorMap tin, T* __restrict__ out, const Mor
           if (k < 0) continue;
           const int r = vy + R + dy;
           uint32_t t;
-          if (k == 0) t = word(stage + r * WBOX, 2 * vq + j);
+          if (k == 0) {
+            if constexpr (sizeof(T) == 2) {
+              t = word(stage + r * WBOX, 2 * vq + j);
+            } else {
+              const uint32_t b4 = *reinterpret_cast<const uint32_t*>(stage + r * WBOX + XA2 + 4 * vq);
+              t = prmt(b4, 0u, j ? 0x4342u : 0x4140u);
+            }
+          }
           else t = sH[((k - 1) * HY + r) * WPR + 2 * vq + j];
           v = op2x2<MAX>(v, t);
         }
