@@ -318,7 +318,13 @@ cudaError_t run_stage(const StageDesc& d, const DevIn& in, int64_t zo, int64_t n
                               d.precision == HB_PREC_EXACT, epi, tmp, s, launches);
     }
     case HB_OP_MEAN: {
-      cudaError_t e = mean_fused(in, zo, nzo, (float*)out, d.radius, s, launches);
+      cudaError_t e = cudaErrorNotSupported;
+      if (!std::getenv("HB_MEAN_TMA")) {
+        e = mean_stream(in, zo, nzo, (float*)out, d.radius, s, launches);
+        if (e != cudaErrorNotSupported) return e;
+        cudaGetLastError();
+      }
+      e = mean_fused(in, zo, nzo, (float*)out, d.radius, s, launches);
       if (e != cudaErrorNotSupported) return e;
       cudaGetLastError();
       float* tmp = (float*)pa.get((size_t)nzo * plane * 4);

@@ -72,6 +72,9 @@ cudaError_t gaussian_exact_fused(const DevIn& in, int64_t zo, int64_t nzo, float
 
 cudaError_t mean_fused(const DevIn& in, int64_t zo, int64_t nzo, float* out, int r,
                        cudaStream_t s, int64_t* launches);
+// streaming box mean, r <= 2, nx % 4 == 0 (box.cu); NotSupported outside that
+cudaError_t mean_stream(const DevIn& in, int64_t zo, int64_t nzo, float* out, int r,
+                        cudaStream_t s, int64_t* launches);
 
 // --- median (median.cu) ----------------------------------------------------
 cudaError_t median(const DevIn& in, int64_t zo, int64_t nzo, void* out, int r,
