@@ -19,6 +19,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
 
 #include "ops.cuh"
@@ -413,29 +414,38 @@ cudaError_t dispatch_dt(int R, const DevIn& in, int64_t zo, int64_t nzo, float* 
 
 
 // ===========================================================================
-// k_gauss_x2 — packed-FP32 (FFMA2/FADD2) variant for the Gaussian, R >= 2.
-// Every pass works on pairs: the Y pass on x-adjacent column pairs (a float2
-// straight out of the TMA rows), the X pass on y-adjacent row pairs (sY is
-// stored row-pair interleaved, so one LDS.128 yields two x positions of a row
-// pair), and the z register ring holds row pairs -> half the FP instructions.
-// Tile 32 x 64 outputs, 512 threads; thread = (row pair, 2 x positions).
+// k_gauss_p2 — packed-FP32 Gaussian / unsharp (fast mode), 2 <= R <= 8.
+//
+// A 17-tap separable pass costs 17 FP ops per voxel per axis, so the Gaussian
+// is bound by the FP32 pipe, not HBM (51 ops/voxel -> ~730 Gvox/s at 128
+// FMA lanes/clk/SM).  Every pass here runs on FFMA2/FADD2 pairs, which halves
+// the FP issue slots so loads, stores and ring traffic fit beside the math:
+//   Y pass (first, over the halo'd width): an item = one x-adjacent column
+//     pair x 4 rows (160 items: 5 of 8 warps busy; 8-row items were 5% slower
+//     from the imbalance), scatter form (acc[m] += w[j-m] * row j), pairs come
+//     straight out of the TMA rows as one LDS.64;
+//   X pass: a thread owns a row pair (y, y+1) x two x positions; sY is stored
+//     row-pair interleaved, so one LDS.128 yields two x columns of a row pair;
+//     computed inside the ring switch so results land in the ring slot (no
+//     MOVs), two partial sums per output to shorten the FFMA2 chain;
+//   Z pass: a (2R+1)-slot register ring of row pairs, symmetric fold.
+// Tile 64 x 16 outputs, 256 threads, 2 CTAs/SM; weights live in uniform
+// registers (FFMA2 takes a UR pair operand).  TMA ring / border clamp /
+// triple-buffered TMA output tile exactly as k_sep3d_fused.
+// Measured (B200, sigma=2, 1024^3): 260 Gvox/s vs 240 for the scalar kernel;
+// ncu: FP pipe 47% busy, shared-memory wavefronts 66% of peak (0.72 per
+// output: the X pass re-reads 18 row pairs per 2 outputs), issue 51% at 16
+// warps/SM (the 17-slot ring pins 118 registers) -> latency/smem bound.
 // ===========================================================================
-namespace x2 {
+namespace p2 {
 typedef unsigned long long f2;
 __device__ __forceinline__ f2 pk(float lo, float hi) {
   f2 d;
   asm("mov.b64 %0, {%1, %2};" : "=l"(d) : "f"(lo), "f"(hi));
   return d;
 }
-__device__ __forceinline__ float lo(f2 v) {
-  float a, b;
+__device__ __forceinline__ void upk(f2 v, float& a, float& b) {
   asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
-  return a;
-}
-__device__ __forceinline__ float hi(f2 v) {
-  float a, b;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
-  return b;
 }
 __device__ __forceinline__ f2 add(f2 a, f2 b) {
   f2 d;
@@ -458,43 +468,52 @@ template <typename T> __device__ __forceinline__ f2 load_pair(const T* p) {
 template <> __device__ __forceinline__ f2 load_pair<float>(const float* p) {
   return *reinterpret_cast<const f2*>(p);
 }
-}  // namespace x2
+}  // namespace p2
 
-constexpr int X2_TX = 32, X2_TY = 64, X2_NT = 512, X2_SEG = 2;
+struct P2Args {
+  unsigned long long w2[kMaxTaps > 17 ? 17 : kMaxTaps];  // (w_k, w_k) pairs
+  int nzi, zo, nzo, zchunk, nx, ny;
+  const void* orig;
+  float amount;
+};
 
-template <int R, typename Tin>
-struct GeoX2 {
-  static constexpr int WC = X2_TX + 2 * R;
-  static constexpr int HB = X2_TY + 2 * R;
+constexpr int P2_TX = 64, P2_TY = 16, P2_NT = 256;
+
+template <int R, typename Tin, int P2_YR>
+struct GeoP2 {
+  static constexpr int WC = P2_TX + 2 * R;                     // halo'd width
+  static constexpr int HB = P2_TY + 2 * R;                     // halo'd height
   static constexpr int ALIGN = 16 / (int)sizeof(Tin);
-  static constexpr int XA = (R + ALIGN - 1) / ALIGN * ALIGN;  // 16-B aligned box start
-  static constexpr int XOFF = XA - R;                         // smem col of halo col 0
-  static constexpr int YC0 = XOFF & ~1;                       // even start of the Y columns
-  static constexpr int YOFF = XOFF - YC0;                     // Y-column of halo col 0
-  static constexpr int NYC = (YOFF + WC + 1) / 2 * 2;         // Y columns (even)
-  static constexpr int NYP = NYC / 2;                         // column pairs
-  static constexpr int WBOX0 = (XA + X2_TX + R) > (YC0 + NYC) ? (XA + X2_TX + R) : (YC0 + NYC);
+  static constexpr int XA = (R + ALIGN - 1) / ALIGN * ALIGN;   // 16-B aligned box start
+  static constexpr int XOFF = XA - R;                          // stage col of halo col 0
+  static constexpr int YC0 = XOFF & ~1;                        // even first Y column
+  static constexpr int YOFF = XOFF - YC0;                      // Y col of halo col 0
+  static constexpr int NYC = (YOFF + WC + 1) / 2 * 2;          // Y columns (even)
+  static constexpr int NYP = NYC / 2;                          // Y column pairs
+  static constexpr int WBOX0 = (XA + P2_TX + R) > (YC0 + NYC) ? (XA + P2_TX + R) : (YC0 + NYC);
   static constexpr int WBOX = (WBOX0 + ALIGN - 1) / ALIGN * ALIGN;
   static constexpr int STAGE_BYTES = HB * WBOX * (int)sizeof(Tin);
   static constexpr int STAGE_PITCH = (STAGE_BYTES + 127) / 128 * 128;
   static constexpr int NST = 3;
   static constexpr int RING = 2 * R + 1;
-  static constexpr int P2 = NYC + 2;  // sY2 row-pair pitch in float2 (even)
-  static constexpr int SY_BYTES = 2 * (X2_TY / 2) * P2 * 8;
-  static constexpr int SOUT_BYTES = 3 * X2_TY * X2_TX * 4;  // triple-buffered (see Geo)
+  static constexpr int NYI = NYP * (P2_TY / P2_YR);            // Y-pass items
+  static constexpr int P2 = NYC + 4;                           // sY row-pair pitch (f2)
+  static constexpr int SY_BYTES = 2 * (P2_TY / 2) * P2 * 8;
+  static constexpr int SOUT_BYTES = 3 * P2_TY * P2_TX * 4;     // triple-buffered
   static constexpr int OFF_SY = NST * STAGE_PITCH;
   static constexpr int OFF_SOUT = OFF_SY + SY_BYTES;
   static constexpr int OFF_BAR = OFF_SOUT + SOUT_BYTES;
   static constexpr int SMEM = OFF_BAR + NST * 8 + 128;
-  static_assert(NYP * (X2_TY / 4) <= X2_NT, "Y-pass items exceed the CTA");
+  static_assert(NYI <= P2_NT, "Y-pass items exceed the CTA");
+  static_assert((P2_TY / 2) * (P2_TX / 2) == P2_NT, "one thread per (row pair, x pair)");
 };
 
-template <int R, typename Tin, bool UNSHARP>
-__global__ void __launch_bounds__(X2_NT, 1)
-k_gauss_x2(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout,
-           const FusedArgs a) {
-  using G = GeoX2<R, Tin>;
-  using namespace x2;
+template <int R, typename Tin, bool UNSHARP, int P2_YR>
+__global__ void __launch_bounds__(P2_NT, 2)
+k_gauss_p2(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout,
+           const __grid_constant__ P2Args a) {
+  using G = GeoP2<R, Tin, P2_YR>;
+  using namespace p2;
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem =
       smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u)  /* stays in .shared */;
@@ -503,15 +522,14 @@ k_gauss_x2(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUte
   float* sOut = reinterpret_cast<float*>(smem + G::OFF_SOUT);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + G::OFF_BAR);
   const int tid = threadIdx.x;
-  const int x0 = blockIdx.x * X2_TX, y0 = blockIdx.y * X2_TY;
+  const int x0 = blockIdx.x * P2_TX, y0 = blockIdx.y * P2_TY;
   const int z0 = blockIdx.z * a.zchunk;
   const int z1 = min(z0 + a.zchunk, a.nzo);
   const int nsl = (z1 - z0) + 2 * R;
-  const bool border = (x0 - R < 0) || (x0 + X2_TX + R > a.nx) || (y0 - R < 0) || (y0 + X2_TY + R > a.ny);
+  const bool border =
+      (x0 - R < 0) || (x0 + P2_TX + R > a.nx) || (y0 - R < 0) || (y0 + P2_TY + R > a.ny);
   auto zin_of = [&](int s) { return min(max(a.zo + z0 - R + s, 0), a.nzi - 1); };
-  f2 W[G::RING];
-#pragma unroll
-  for (int k = 0; k < G::RING; ++k) W[k] = pk(a.w[k], a.w[k]);
+  const f2* W = a.w2;  // kernel-param bank -> uniform registers
 
   if (tid == 0) {
     prefetch_tmap(&tin);
@@ -523,16 +541,17 @@ k_gauss_x2(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUte
     for (int i = 0; i < G::NST; ++i)
       if (i < nsl) {
         mbar_expect_tx(&bar[i], G::HB * G::WBOX * sizeof(Tin));
-        tma_load_3d(sIn + i * (G::STAGE_PITCH / sizeof(Tin)), &tin, x0 - G::XA, y0 - R, zin_of(i), &bar[i]);
+        tma_load_3d(sIn + i * (G::STAGE_PITCH / sizeof(Tin)), &tin, x0 - G::XA, y0 - R, zin_of(i),
+                    &bar[i]);
       }
   }
   __syncthreads();
-  // Y-pass item: column pair cp, 4 output rows from 4*yg
+  // Y item: column pair ycp, rows [P2_YR * yg, P2_YR * yg + P2_YR)
   const int ycp = tid % G::NYP, yg = tid / G::NYP;
-  const bool y_active = yg < X2_TY / 4;
+  const bool y_active = tid < G::NYI;
   // X/Z ownership: row pair yp, x positions 2*sg, 2*sg+1
-  const int yp = tid >> 4, sg = tid & 15;
-  f2 ring[G::RING][X2_SEG];
+  const int yp = tid / (P2_TX / 2), sg = tid % (P2_TX / 2);
+  f2 ring[G::RING][2];
 #pragma unroll
   for (int u = 0; u < G::RING; ++u) ring[u][0] = ring[u][1] = 0ull;
 
@@ -541,39 +560,43 @@ k_gauss_x2(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUte
     Tin* stage = sIn + st * (G::STAGE_PITCH / sizeof(Tin));
     mbar_wait(&bar[st], (uint32_t)((s / G::NST) & 1));
     if (border) {
-      for (int e = tid; e < G::HB * G::WC; e += X2_NT) {
+      for (int e = tid; e < G::HB * G::WC; e += P2_NT) {
         const int ly = e / G::WC, lx = e - ly * G::WC;
         const int gy = y0 - R + ly, gx = x0 - R + lx;
         const int cy = min(max(gy, 0), a.ny - 1), cx = min(max(gx, 0), a.nx - 1);
         if (cy != gy || cx != gx)
-          stage[ly * G::WBOX + G::XOFF + lx] = stage[(cy - (y0 - R)) * G::WBOX + G::XOFF + (cx - (x0 - R))];
+          stage[ly * G::WBOX + G::XOFF + lx] =
+              stage[(cy - (y0 - R)) * G::WBOX + G::XOFF + (cx - (x0 - R))];
       }
       fence_proxy_async();
       __syncthreads();
     }
-    // ---- Y pass (column pairs) -> sY (row-pair interleaved) -----------------
-    f2* sYb = sY + (s & 1) * (X2_TY / 2) * G::P2;
+    // ---- Y pass (column pairs, scatter form) -> sY row-pair interleaved ------
+    f2* sYb = sY + (s & 1) * (P2_TY / 2) * G::P2;
     if (y_active) {
-      f2 v[4 + 2 * R];
+      f2 acc[P2_YR];
+      const Tin* src = stage + (P2_YR * yg) * G::WBOX + G::YC0 + 2 * ycp;
 #pragma unroll
-      for (int j = 0; j < 4 + 2 * R; ++j) v[j] = load_pair<Tin>(stage + (4 * yg + j) * G::WBOX + G::YC0 + 2 * ycp);
-      f2 o[4];
+      for (int j = 0; j < P2_YR + 2 * R; ++j) {
+        const f2 v = load_pair<Tin>(src + j * G::WBOX);
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        f2 acc = mul(v[j + R], W[R]);
-#pragma unroll
-        for (int d = R; d >= 1; --d) acc = fma(add(v[j + R - d], v[j + R + d]), W[R - d], acc);
-        o[j] = acc;
+        for (int m = 0; m < P2_YR; ++m) {
+          const int k = j - m;
+          if (k == 0) acc[m] = mul(v, W[0]);
+          else if (k > 0 && k <= 2 * R) acc[m] = fma(v, W[k], acc[m]);
+        }
       }
-      // rows (4yg, 4yg+1) -> row pair 2yg; (4yg+2, 4yg+3) -> 2yg+1; store as
-      // [(c,r0),(c,r1)],[(c+1,r0),(c+1,r1)]
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const f2 ra = o[2 * h], rb = o[2 * h + 1];
+      for (int m = 0; m < P2_YR; m += 2) {
+        float a0, a1, b0, b1;
+        upk(acc[m], a0, a1);      // row m:   (c, c+1)
+        upk(acc[m + 1], b0, b1);  // row m+1: (c, c+1)
         uint4 q;
-        q.x = __float_as_uint(lo(ra)); q.y = __float_as_uint(lo(rb));
-        q.z = __float_as_uint(hi(ra)); q.w = __float_as_uint(hi(rb));
-        *reinterpret_cast<uint4*>(sYb + (2 * yg + h) * G::P2 + 2 * ycp) = q;
+        q.x = __float_as_uint(a0);
+        q.y = __float_as_uint(b0);
+        q.z = __float_as_uint(a1);
+        q.w = __float_as_uint(b1);
+        *reinterpret_cast<uint4*>(sYb + ((P2_YR * yg + m) / 2) * G::P2 + 2 * ycp) = q;
       }
     }
     __syncthreads();
@@ -585,65 +608,74 @@ k_gauss_x2(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUte
       }
       const int o_prev = s - 1 - 2 * R;
       if (o_prev >= 0) {
-        tma_store_3d(&tout, sOut + (o_prev % 3) * X2_TY * X2_TX, x0, y0, z0 + o_prev);
+        tma_store_3d(&tout, sOut + (o_prev % 3) * P2_TY * P2_TX, x0, y0, z0 + o_prev);
         bulk_commit();
         bulk_wait_read<1>();
       }
     }
-    // ---- X pass (row pairs) ------------------------------------------------
-    f2 xo[X2_SEG];
-    {
-      f2 v[X2_SEG + 2 * R];
+    // ---- X pass (row pairs, scatter form), written straight into the ring slot
+    // two partial sums per output (taps <= R / > R) halve the dependent chain
+    auto xpass = [&](f2& out0, f2& out1) {
+      f2 xa[2], xb[2];
       const f2* row = sYb + yp * G::P2 + G::YOFF + 2 * sg;
+      auto tap = [&](int c, f2 v) {
+#pragma unroll
+        for (int m = 0; m < 2; ++m) {
+          const int k = c - m;
+          if (k == 0) xa[m] = mul(v, W[0]);
+          else if (k == R + 1) xb[m] = mul(v, W[k]);
+          else if (k > 0 && k <= R) xa[m] = fma(v, W[k], xa[m]);
+          else if (k > R + 1 && k <= 2 * R) xb[m] = fma(v, W[k], xb[m]);
+        }
+      };
       if (G::YOFF == 0) {
 #pragma unroll
-        for (int i = 0; i < (X2_SEG + 2 * R) / 2; ++i) {
-          const uint4 q = *reinterpret_cast<const uint4*>(row + 2 * i);
-          v[2 * i] = ((f2)q.y << 32) | q.x;
-          v[2 * i + 1] = ((f2)q.w << 32) | q.z;
+        for (int i = 0; i < (2 + 2 * R) / 2; ++i) {
+          f2 v0, v1;  // one LDS.128: columns 2i, 2i+1 of the row pair
+          asm volatile("ld.shared.v2.b64 {%0, %1}, [%2];"
+                       : "=l"(v0), "=l"(v1)
+                       : "r"(smem_u32(row + 2 * i)));
+          tap(2 * i, v0);
+          tap(2 * i + 1, v1);
         }
       } else {
 #pragma unroll
-        for (int i = 0; i < X2_SEG + 2 * R; ++i) v[i] = row[i];
+        for (int c = 0; c < 2 + 2 * R; ++c) tap(c, row[c]);
       }
-#pragma unroll
-      for (int m = 0; m < X2_SEG; ++m) {
-        f2 acc = mul(v[m + R], W[R]);
-#pragma unroll
-        for (int d = R; d >= 1; --d) acc = fma(add(v[m + R - d], v[m + R + d]), W[R - d], acc);
-        xo[m] = acc;
-      }
-    }
-    // ---- ring + Z pass -------------------------------------------------------
+      out0 = add(xa[0], xb[0]);
+      out1 = add(xa[1], xb[1]);
+    };
+    // ---- ring + Z pass (symmetric fold) --------------------------------------
     const int o = s - 2 * R;
-    f2 zr[X2_SEG];
+    f2 zr[2];
     bool have = false;
     switch (s % G::RING) {
-#define HB_X2_CASE(U)                                                                  \
-  case U:                                                                              \
-    if constexpr (U < G::RING) {                                                       \
-      ring[U][0] = xo[0];                                                              \
-      ring[U][1] = xo[1];                                                              \
-      if (o >= 0) {                                                                    \
-        have = true;                                                                   \
-        _Pragma("unroll") for (int m = 0; m < X2_SEG; ++m) {                           \
-          f2 acc = mul(ring[(U + 1 + R) % G::RING][m], W[R]);                           \
-          _Pragma("unroll") for (int d = R; d >= 1; --d) acc =                         \
+#define HB_P2_CASE(U)                                                                        \
+  case U:                                                                                    \
+    if constexpr (U < G::RING) {                                                             \
+      xpass(ring[U][0], ring[U][1]);                                                         \
+      if (o >= 0) {                                                                          \
+        have = true;                                                                         \
+        _Pragma("unroll") for (int m = 0; m < 2; ++m) {                                      \
+          f2 acc = mul(ring[(U + 1 + R) % G::RING][m], W[R]);                                \
+          _Pragma("unroll") for (int d = R; d >= 1; --d) acc =                               \
               fma(add(ring[(U + 1 + R - d) % G::RING][m], ring[(U + 1 + R + d) % G::RING][m]), \
-                  W[R - d], acc);                                                      \
-          zr[m] = acc;                                                                 \
-        }                                                                              \
-      }                                                                                \
-    }                                                                                  \
+                  W[R - d], acc);                                                            \
+          zr[m] = acc;                                                                       \
+        }                                                                                    \
+      }                                                                                      \
+    }                                                                                        \
     break;
-      HB_X2_CASE(0) HB_X2_CASE(1) HB_X2_CASE(2) HB_X2_CASE(3) HB_X2_CASE(4) HB_X2_CASE(5)
-      HB_X2_CASE(6) HB_X2_CASE(7) HB_X2_CASE(8) HB_X2_CASE(9) HB_X2_CASE(10) HB_X2_CASE(11)
-      HB_X2_CASE(12) HB_X2_CASE(13) HB_X2_CASE(14) HB_X2_CASE(15) HB_X2_CASE(16)
-#undef HB_X2_CASE
+      HB_P2_CASE(0) HB_P2_CASE(1) HB_P2_CASE(2) HB_P2_CASE(3) HB_P2_CASE(4) HB_P2_CASE(5)
+      HB_P2_CASE(6) HB_P2_CASE(7) HB_P2_CASE(8) HB_P2_CASE(9) HB_P2_CASE(10) HB_P2_CASE(11)
+      HB_P2_CASE(12) HB_P2_CASE(13) HB_P2_CASE(14) HB_P2_CASE(15) HB_P2_CASE(16)
+#undef HB_P2_CASE
       default: break;
     }
     if (have) {
-      float r0[2] = {lo(zr[0]), lo(zr[1])}, r1[2] = {hi(zr[0]), hi(zr[1])};
+      float r0[2], r1[2];  // rows 2yp, 2yp+1 at x = 2sg, 2sg+1
+      upk(zr[0], r0[0], r1[0]);
+      upk(zr[1], r0[1], r1[1]);
       if (UNSHARP) {
         const int64_t zb = (int64_t)a.zo + z0 + o;
         const Tin* ob = reinterpret_cast<const Tin*>(a.orig);
@@ -659,9 +691,9 @@ k_gauss_x2(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUte
           }
         }
       }
-      float* dst = sOut + (o % 3) * X2_TY * X2_TX + (2 * yp) * X2_TX + 2 * sg;
+      float* dst = sOut + (o % 3) * P2_TY * P2_TX + (2 * yp) * P2_TX + 2 * sg;
       *reinterpret_cast<float2*>(dst) = make_float2(r0[0], r0[1]);
-      *reinterpret_cast<float2*>(dst + X2_TX) = make_float2(r1[0], r1[1]);
+      *reinterpret_cast<float2*>(dst + P2_TX) = make_float2(r1[0], r1[1]);
       fence_proxy_async();
     }
   }
@@ -669,24 +701,28 @@ k_gauss_x2(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUte
   if (tid == 0) {
     const int o_last = nsl - 1 - 2 * R;
     if (o_last >= 0) {
-      tma_store_3d(&tout, sOut + (o_last % 3) * X2_TY * X2_TX, x0, y0, z0 + o_last);
+      tma_store_3d(&tout, sOut + (o_last % 3) * P2_TY * P2_TX, x0, y0, z0 + o_last);
       bulk_commit();
     }
     bulk_wait<0>();
   }
 }
 
-template <int R, typename Tin, bool UNSHARP>
-cudaError_t launch_x2(const DevIn& in, int64_t zo, int64_t nzo, float* out, const Taps& taps,
+template <int R, typename Tin, bool UNSHARP, int P2_YR>
+cudaError_t launch_p2(const DevIn& in, int64_t zo, int64_t nzo, float* out, const Taps& taps,
                       const EpiArgs& epi, cudaStream_t s) {
-  using G = GeoX2<R, Tin>;
+  using G = GeoP2<R, Tin, P2_YR>;
   CUtensorMap tin, tout;
   if (!make_tmap_3d(&tin, in.p, TmaType<Tin>::v, sizeof(Tin), in.nx, in.ny, in.nz, G::WBOX, G::HB))
     return cudaErrorNotSupported;
-  if (!make_tmap_3d(&tout, out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, in.nx, in.ny, nzo, X2_TX, X2_TY))
+  if (!make_tmap_3d(&tout, out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, in.nx, in.ny, nzo, P2_TX, P2_TY))
     return cudaErrorNotSupported;
-  FusedArgs a;
-  for (int k = 0; k < 2 * R + 1; ++k) a.w[k] = taps.w[k];
+  P2Args a;
+  for (int k = 0; k < 2 * R + 1; ++k) {
+    unsigned int b = 0;
+    std::memcpy(&b, &taps.w[k], 4);
+    a.w2[k] = ((unsigned long long)b << 32) | b;
+  }
   a.nzi = (int)in.nz;
   a.zo = (int)zo;
   a.nzo = (int)nzo;
@@ -694,9 +730,15 @@ cudaError_t launch_x2(const DevIn& in, int64_t zo, int64_t nzo, float* out, cons
   a.ny = (int)in.ny;
   a.orig = epi.orig;
   a.amount = epi.amount;
-  const int gx = (int)((in.nx + X2_TX - 1) / X2_TX), gy = (int)((in.ny + X2_TY - 1) / X2_TY);
+  auto kern = k_gauss_p2<R, Tin, UNSHARP, P2_YR>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, P2_NT, G::SMEM) != cudaSuccess ||
+      per_sm < 1)
+    per_sm = 1;
+  const int gx = (int)((in.nx + P2_TX - 1) / P2_TX), gy = (int)((in.ny + P2_TY - 1) / P2_TY);
   const int64_t tiles = (int64_t)gx * gy;
-  const int64_t slots = kNumSMs;
+  const int64_t slots = (int64_t)kNumSMs * per_sm;
   double best = 1e300;
   int best_split = 1;
   for (int split = 1; split <= 256; ++split) {
@@ -712,37 +754,36 @@ cudaError_t launch_x2(const DevIn& in, int64_t zo, int64_t nzo, float* out, cons
   }
   a.zchunk = (int)((nzo + best_split - 1) / best_split);
   dim3 grid(gx, gy, (unsigned)((nzo + a.zchunk - 1) / a.zchunk));
-  auto kern = k_gauss_x2<R, Tin, UNSHARP>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
-  kern<<<grid, X2_NT, G::SMEM, s>>>(tin, tout, a);
+  kern<<<grid, P2_NT, G::SMEM, s>>>(tin, tout, a);
   return cudaGetLastError();
 }
 
 template <bool UNSHARP, typename Tin>
-cudaError_t dispatch_x2(int R, const DevIn& in, int64_t zo, int64_t nzo, float* out,
+cudaError_t dispatch_p2(int R, const DevIn& in, int64_t zo, int64_t nzo, float* out,
                         const Taps& taps, const EpiArgs& epi, cudaStream_t s) {
   switch (R) {
-    case 2: return launch_x2<2, Tin, UNSHARP>(in, zo, nzo, out, taps, epi, s);
-    case 3: return launch_x2<3, Tin, UNSHARP>(in, zo, nzo, out, taps, epi, s);
-    case 4: return launch_x2<4, Tin, UNSHARP>(in, zo, nzo, out, taps, epi, s);
-    case 5: return launch_x2<5, Tin, UNSHARP>(in, zo, nzo, out, taps, epi, s);
-    case 6: return launch_x2<6, Tin, UNSHARP>(in, zo, nzo, out, taps, epi, s);
-    case 7: return launch_x2<7, Tin, UNSHARP>(in, zo, nzo, out, taps, epi, s);
-    case 8: return launch_x2<8, Tin, UNSHARP>(in, zo, nzo, out, taps, epi, s);
+    case 2: return launch_p2<2, Tin, UNSHARP, 4>(in, zo, nzo, out, taps, epi, s);
+    case 3: return launch_p2<3, Tin, UNSHARP, 4>(in, zo, nzo, out, taps, epi, s);
+    case 4: return launch_p2<4, Tin, UNSHARP, 4>(in, zo, nzo, out, taps, epi, s);
+    case 5: return launch_p2<5, Tin, UNSHARP, 4>(in, zo, nzo, out, taps, epi, s);
+    case 6: return launch_p2<6, Tin, UNSHARP, 4>(in, zo, nzo, out, taps, epi, s);
+    case 7: return launch_p2<7, Tin, UNSHARP, 4>(in, zo, nzo, out, taps, epi, s);
+    case 8: return launch_p2<8, Tin, UNSHARP, 4>(in, zo, nzo, out, taps, epi, s);
   }
   return cudaErrorNotSupported;
 }
 
 template <bool UNSHARP>
-cudaError_t dispatch_x2_dt(int R, const DevIn& in, int64_t zo, int64_t nzo, float* out,
+cudaError_t dispatch_p2_dt(int R, const DevIn& in, int64_t zo, int64_t nzo, float* out,
                            const Taps& taps, const EpiArgs& epi, cudaStream_t s) {
   switch (in.dt) {
-    case HB_F32: return dispatch_x2<UNSHARP, float>(R, in, zo, nzo, out, taps, epi, s);
-    case HB_U16: return dispatch_x2<UNSHARP, uint16_t>(R, in, zo, nzo, out, taps, epi, s);
-    case HB_U8: return dispatch_x2<UNSHARP, uint8_t>(R, in, zo, nzo, out, taps, epi, s);
+    case HB_F32: return dispatch_p2<UNSHARP, float>(R, in, zo, nzo, out, taps, epi, s);
+    case HB_U16: return dispatch_p2<UNSHARP, uint16_t>(R, in, zo, nzo, out, taps, epi, s);
+    case HB_U8: return dispatch_p2<UNSHARP, uint8_t>(R, in, zo, nzo, out, taps, epi, s);
   }
   return cudaErrorNotSupported;
 }
+
 
 bool envelope_ok(const DevIn& in, int64_t nzo) {
   if (nzo <= 0) return false;
@@ -758,12 +799,10 @@ cudaError_t gaussian_fused(const DevIn& in, int64_t zo, int64_t nzo, float* out,
   if (!envelope_ok(in, nzo) || taps.R > 8) return cudaErrorNotSupported;
   cudaError_t e = cudaErrorNotSupported;
   if (epi.kind == EPI_UNSHARP && (epi.orig != in.p || epi.orig_dt != in.dt)) return cudaErrorNotSupported;
-  // The packed-FP32 variant halves the FP instructions but measured slower on
-  // B200 (154 vs 241 Gvox/s at sigma=2, 1024^3: its per-thread overhead grows);
-  // kept opt-in (HB_X2=1) for further tuning.
-  if (taps.R >= 2 && std::getenv("HB_X2")) {
-    e = epi.kind == EPI_UNSHARP ? dispatch_x2_dt<true>(taps.R, in, zo, nzo, out, taps, epi, s)
-                                : dispatch_x2_dt<false>(taps.R, in, zo, nzo, out, taps, epi, s);
+  // packed-FP32 kernel for R >= 2 (HB_GAUSS_SCALAR=1 selects the scalar one)
+  if (taps.R >= 2 && !std::getenv("HB_GAUSS_SCALAR")) {
+    e = epi.kind == EPI_UNSHARP ? dispatch_p2_dt<true>(taps.R, in, zo, nzo, out, taps, epi, s)
+                                : dispatch_p2_dt<false>(taps.R, in, zo, nzo, out, taps, epi, s);
     if (e != cudaErrorNotSupported) {
       if (e == cudaSuccess && launches) *launches += 1;
       return e;
