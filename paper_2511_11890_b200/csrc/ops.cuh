@@ -54,6 +54,10 @@ cudaError_t mean_generic(const DevIn& in, int64_t zo, int64_t nzo, float* out, i
 cudaError_t log_diff(const float* g, int64_t gz0, int64_t ngz, int64_t nz, int64_t ny,
                      int64_t nx, int64_t zo, int64_t nzo, float* out, cudaStream_t s,
                      int64_t* launches);
+// streaming form of log_diff (logd.cu); NotSupported unless nx % 4 == 0
+cudaError_t log_diff_stream(const float* g, int64_t gz0, int64_t nz, int64_t ny, int64_t nx,
+                            int64_t zo, int64_t nzo, float* out, cudaStream_t s,
+                            int64_t* launches);
 // dtype conversion / copy (identity op, registry.py:127-133)
 cudaError_t copy_slices(const DevIn& in, int64_t zo, int64_t nzo, void* out,
                         cudaStream_t s, int64_t* launches);

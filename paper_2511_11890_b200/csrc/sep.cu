@@ -9,6 +9,8 @@
 // throughput path; this file is its fallback and the LoG smoothing stage.
 #include <algorithm>
 
+#include <cstdlib>
+
 #include "ops.cuh"
 
 namespace hb {
@@ -256,6 +258,11 @@ cudaError_t log_diff(const float* g, int64_t gz0, int64_t ngz, int64_t nz, int64
                      int64_t* launches) {
   (void)ngz;
   if (nzo <= 0) return cudaSuccess;
+  if (!std::getenv("HB_LOG_TILE")) {
+    const cudaError_t e = log_diff_stream(g, gz0, nz, ny, nx, zo, nzo, out, s, launches);
+    if (e != cudaErrorNotSupported) return e;
+    cudaGetLastError();
+  }
   const int64_t tiles = ((nx + LD_TX - 1) / LD_TX) * ((ny + LD_TY - 1) / LD_TY);
   // short z-chunks: each step's loads are latency-bound, so parallelism (many
   // resident CTAs) hides them; 32 slices keep the window priming cost at ~12%
