@@ -280,3 +280,26 @@ def test_pinned_context_direct_dma(hb):
     with pinned(x, out):
         got, rep = registry.run_operator(x, "median", {"radius": 1}, b, out=out)
     assert got is out and np.array_equal(out, want) and rep.device_residual_bytes == 0
+
+
+STREAM_SHAPES = [(21, 37, 132), (9, 70, 260), (5, 3, 516), (12, 130, 128), (2, 9, 4)]
+
+
+@pytest.mark.parametrize("shape", STREAM_SHAPES)
+def test_streaming_kernels_vs_oracle(hb, oracle, shape):
+    """Shapes that exercise the streaming kernels' strip tails and faces
+    (box.cu mean, logd.cu LoG stage, k_gauss_p2): x = 128k + 4 (one live lane in
+    the last strip), tiny y, ny < the warp's row block, nz < 2R+1."""
+    from paper_2511_11890_b200 import filters
+
+    rng = np.random.default_rng(sum(shape))
+    for dt in ("f32", "u16", "u8"):
+        x = _vol(rng, shape, dt)
+        assert float_close(filters.mean(x, 1), oracle.mean(x, 1)) <= FLOAT_TOL, dt
+        assert float_close(filters.mean(x, 2), oracle.mean(x, 2)) <= FLOAT_TOL, dt
+        assert float_close(filters.gaussian(x, 2.0), oracle.gaussian(x, 2.0)) <= FLOAT_TOL, dt
+        assert float_close(filters.unsharp(x, 1.0, 1.5), oracle.unsharp(x, 1.0, 1.5)) <= FLOAT_TOL, dt
+    x = _vol(rng, shape, "f32")
+    assert np.array_equal(filters.log(x, 2.0), oracle.log(x, 2.0))
+    xi = _vol(rng, shape, "u16")
+    assert np.array_equal(filters.mean(xi, 1), oracle.mean(xi, 1))  # integer sums: exact
