@@ -166,6 +166,14 @@ int32_t hb_chain_out_dtype(const hb_stage* stages, int32_t nstages, int32_t in_d
 /* Trim the library's private device pool of `dev` to zero bytes (after
  * asynchronous hb_apply_device calls; synchronous jobs trim themselves). */
 int32_t hb_trim_device(int32_t dev);
+/* Device-arena session (extension; no reference counterpart): between
+ * hb_session_begin(dev) and the matching hb_session_end(dev), jobs on `dev`
+ * return their buffers to the library pool without trimming it, so repeated
+ * jobs skip the driver's map/unmap; hb_session_end trims the pool to zero.
+ * Nested sessions are counted.  Outside a session every job trims itself
+ * (chunking.py's job-scoped reservation, chunking.py:243). */
+int32_t hb_session_begin(int32_t dev);
+int32_t hb_session_end(int32_t dev);
 /* Bytes currently reserved by the library's private pool on `dev`. */
 int64_t hb_device_pool_bytes(int32_t dev);
 

@@ -110,6 +110,7 @@ EXPORTS = (
     "hb_gaussian_radius", "hb_gaussian_weights", "hb_chain_halo", "hb_run",
     "hb_apply_device", "hb_chain_out_dtype", "hb_trim_device",
     "hb_device_pool_bytes", "hb_pin", "hb_unpin", "hb_last_error",
+    "hb_session_begin", "hb_session_end",
 )
 
 _lock = threading.Lock()
@@ -154,6 +155,10 @@ def load() -> ctypes.CDLL:
         L.hb_trim_device.restype = i32
         L.hb_device_pool_bytes.argtypes = [i32]
         L.hb_device_pool_bytes.restype = i64
+        L.hb_session_begin.argtypes = [i32]
+        L.hb_session_begin.restype = i32
+        L.hb_session_end.argtypes = [i32]
+        L.hb_session_end.restype = i32
         L.hb_pin.argtypes = [vp, i64]
         L.hb_pin.restype = i32
         L.hb_unpin.argtypes = [vp]
@@ -368,6 +373,32 @@ def trim_device(dev: Optional[int] = None) -> None:
 
 def device_pool_bytes(dev: Optional[int] = None) -> int:
     return int(load().hb_device_pool_bytes(current_device() if dev is None else int(dev)))
+
+
+class session:
+    """Device-arena session: jobs inside the ``with`` block keep the library's
+    device pool mapped between calls (each job still frees every buffer it
+    allocated: ``ExecutionReport.device_residual_bytes`` stays 0), and the
+    pool is trimmed to zero when the block exits.  Use it around a series of
+    ``run_operator`` calls; a single call releases all device memory itself::
+
+        with session(), pinned(volume, out):
+            for name, p in steps:
+                registry.run_operator(volume, name, p, budget, out=out)
+    """
+
+    def __init__(self, dev: Optional[int] = None):
+        self.dev = dev
+
+    def __enter__(self):
+        L = load()
+        self._dev = current_device() if self.dev is None else int(self.dev)
+        raise_for_status(L.hb_session_begin(self._dev), last_error())
+        return self
+
+    def __exit__(self, *exc):
+        load().hb_session_end(self._dev)
+        return False
 
 
 class pinned:

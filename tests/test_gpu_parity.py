@@ -303,3 +303,20 @@ def test_streaming_kernels_vs_oracle(hb, oracle, shape):
     assert np.array_equal(filters.log(x, 2.0), oracle.log(x, 2.0))
     xi = _vol(rng, shape, "u16")
     assert np.array_equal(filters.mean(xi, 1), oracle.mean(xi, 1))  # integer sums: exact
+
+
+def test_device_session_keeps_pool_until_exit(hb):
+    """hb_session_begin/end: jobs inside a session free every buffer (job
+    residual 0) but leave the pool mapped; leaving the session trims it."""
+    from paper_2511_11890_b200 import _native, registry, session
+
+    x = np.random.default_rng(5).random((24, 64, 64), dtype=np.float32)
+    _, rep = registry.run_operator(x, "median", {"radius": 1})
+    assert rep.device_residual_bytes == 0 and _native.device_pool_bytes() == 0
+    with session():
+        a, r1 = registry.run_operator(x, "median", {"radius": 1})
+        b, r2 = registry.run_operator(x, "mean", {"radius": 1})
+        assert r1.device_residual_bytes == 0 and r2.device_residual_bytes == 0
+        assert _native.device_pool_bytes() > 0
+    assert _native.device_pool_bytes() == 0
+    assert np.array_equal(a, registry.run_operator(x, "median", {"radius": 1})[0])
