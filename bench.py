@@ -311,7 +311,7 @@ def run_ours(args):
     tr = traffic_from_profiles().get(dominant)
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": tr,
-                "kernel": f"{dominant} r=1 ({'k_median3_plane' if dominant == 'median' else 'k_sep3d_fused<1,float,BOX>'})",
+                "kernel": f"{dominant} r=1 ({'k_median3_plane' if dominant == 'median' else 'k_box_stream<float,1>'})",
                 "peak_kind": peak_kind,
                 "algorithmic_bytes_per_launch": BYTES_PER_VOXEL * vox}
     filters_out = {

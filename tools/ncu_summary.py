@@ -23,6 +23,9 @@ METRICS = [
     ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue active %"),
     ("sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active", "FMA pipe %"),
     ("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active", "ALU pipe %"),
+    ("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", "FMA pipe cycles %"),
+    ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "FP64 pipe cycles %"),
+    ("l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed", "LSU wavefronts % (smem+L1)"),
     ("smsp__inst_executed.sum", "warp instructions"),
     ("smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio", "stall long_scoreboard"),
     ("smsp__average_warps_issue_stalled_wait_per_issue_active.ratio", "stall wait"),
@@ -32,8 +35,9 @@ METRICS = [
     ("smsp__average_warps_issue_stalled_short_scoreboard_per_issue_active.ratio", "stall short_scoreboard"),
 ]
 
-KEYS = {"k_median3_plane": "median", "k_sep3d_fused<1": "mean", "k_sep3d_fused<8": "gaussian",
-        "k_morph": "erode", "k_axis_pass": "generic_pass"}
+KEYS = {"k_median3_plane": "median", "k_box_stream": "mean", "k_gauss_p2<8": "gaussian",
+        "k_morph3": "erode", "k_log_stream": "log_stage2", "k_exact_z<8": "exact_z",
+        "k_exact_yx<8": "exact_yx"}
 
 
 def main(rep, out_md):
