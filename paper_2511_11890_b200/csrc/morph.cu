@@ -542,6 +542,38 @@ __device__ __forceinline__ uint32_t op3x2(uint32_t a, uint32_t b, uint32_t c) {
   return op2x2<MAX>(op2x2<MAX>(a, b), c);  // ptxas fuses into VIMNMX3.U16x2
 }
 
+// Clamp-to-edge fix-up of a TMA-staged halo'd tile whose out-of-volume parts
+// TMA zero-filled: out-of-range rows are copied whole from the nearest valid
+// row, then out-of-range columns of every row from the nearest valid column.
+// Touches only the halo strips (the per-element loop over the whole tile it
+// replaces was ~20% of k_morph3's instructions at 1024^3).  The caller fences
+// and synchronises afterwards.
+template <typename T, int NT>
+__device__ __forceinline__ void clamp_tile(T* st, int pitch, int h, int w, int gy0, int gx0, int ny,
+                                           int nx, int tid) {
+  const int r_lo = max(0, -gy0), r_hi = min(h, ny - gy0);
+  if (r_lo > 0 || r_hi < h) {
+    const int nbad = r_lo + (h - r_hi);
+    for (int e = tid; e < nbad * w; e += NT) {
+      const int i = e / w, c = e - i * w;
+      const int r = i < r_lo ? i : r_hi + (i - r_lo);
+      const int src = i < r_lo ? r_lo : r_hi - 1;
+      st[r * pitch + c] = st[src * pitch + c];
+    }
+    __syncthreads();
+  }
+  const int c_lo = max(0, -gx0), c_hi = min(w, nx - gx0);
+  if (c_lo > 0 || c_hi < w) {
+    const int nbc = c_lo + (w - c_hi);
+    for (int e = tid; e < h * nbc; e += NT) {
+      const int r = e / nbc, i = e - r * nbc;
+      const int c = i < c_lo ? i : c_hi + (i - c_lo);
+      const int src = i < c_lo ? c_lo : c_hi - 1;
+      st[r * pitch + c] = st[r * pitch + src];
+    }
+  }
+}
+
 template <typename T, bool MAX, int KIND, int R>
 __global__ void __launch_bounds__(M3X_NT, 2)
 k_morph3(const __grid_constant__ CUtensorMap tin, T* __restrict__ out, const Morph3Args a) {
@@ -598,24 +630,39 @@ k_morph3(const __grid_constant__ CUtensorMap tin, T* __restrict__ out, const Mor
     }
   };
 
+  // output pointer of local output slice 0 and this thread's store shape
+  const int gy = y0 + vy, gx = x0 + 4 * vq;
+  const bool st_full = gy < a.ny && gx + 3 < a.nx;
+  const bool st_part = gy < a.ny && gx < a.nx && !st_full;
+  T* const obase = out + ((int64_t)z0 * a.ny + min(gy, a.ny - 1)) * (int64_t)a.nx + min(gx, a.nx - 1);
+  const int64_t oplane = (int64_t)a.ny * a.nx;
+  auto store_out = [&](int o, uint32_t v0, uint32_t v1) {
+    T* dst = obase + o * oplane;
+    if (st_full) {
+      if constexpr (sizeof(T) == 2) *reinterpret_cast<uint2*>(dst) = make_uint2(v0, v1);
+      else *reinterpret_cast<uint32_t*>(dst) = prmt(v0, v1, 0x6420);
+    } else if (st_part) {
+      const uint32_t vv[2] = {v0, v1};
+      for (int i = 0; i < 4 && gx + i < a.nx; ++i) dst[i] = (T)((vv[i >> 1] >> (16 * (i & 1))) & 0xffffu);
+    }
+  };
+
   for (int s = 0; s < nsl; ++s) {
     const int st = s % M3X_NST;
     T* stage = sraw + st * (STAGE_PITCH / sizeof(T));
     mbar_wait(&bar[st], (uint32_t)((s / M3X_NST) & 1));
     if (border) {
-      constexpr int WC = M3X_TX + 2 * XA2;
-      for (int e = tid; e < HY * WC; e += M3X_NT) {
-        const int ly = e / WC, lx = e - ly * WC;
-        const int gy = y0 - R + ly, gx = x0 - XA2 + lx;
-        const int cy = min(max(gy, 0), a.ny - 1), cx = min(max(gx, 0), a.nx - 1);
-        if (cy != gy || cx != gx) stage[ly * WBOX + lx] = stage[(cy - (y0 - R)) * WBOX + (cx - (x0 - XA2))];
-      }
+      clamp_tile<T, M3X_NT>(stage, WBOX, HY, M3X_TX + 2 * XA2, y0 - R, x0 - XA2, a.ny, a.nx, tid);
       fence_proxy_async();
       __syncthreads();
     }
     // ---- H: run reductions for every halo'd row -----------------------------
     if constexpr (R > 0) {
-      for (int item = tid; item < HY * M3X_Q; item += M3X_NT) {
+      // a compile-time trip count lets the per-item index math hoist out of the slice loop
+#pragma unroll
+      for (int it = 0; it < (HY * M3X_Q + M3X_NT - 1) / M3X_NT; ++it) {
+        const int item = tid + it * M3X_NT;
+        if (item >= HY * M3X_Q) break;
         const int r = item / M3X_Q, q = item % M3X_Q;
         const T* row = stage + r * WBOX;
         uint32_t w[6];  // pairs 2q-2 .. 2q+3
@@ -652,66 +699,70 @@ k_morph3(const __grid_constant__ CUtensorMap tin, T* __restrict__ out, const Mor
     }
     __syncthreads();
     // ---- V: every layer's 2D shape for this thread's 4 outputs ----------------
+    // rows of one layer are folded three at a time (VIMNMX3.U16x2); the two
+    // words of a row come from one LDS.64; identical loads across layers CSE
     uint32_t layer[R + 1][2];
-#pragma unroll
-    for (int L = 0; L <= R; ++L) {
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        uint32_t v = IDENT;
-#pragma unroll
-        for (int dy = -R; dy <= R; ++dy) {
-          const int k = S::hw(L, dy);
-          if (k < 0) continue;
-          const int r = vy + R + dy;
-          uint32_t t;
-          if (k == 0) {
-            if constexpr (sizeof(T) == 2) {
-              t = word(stage + r * WBOX, 2 * vq + j);
-            } else {
-              const uint32_t b4 = *reinterpret_cast<const uint32_t*>(stage + r * WBOX + XA2 + 4 * vq);
-              t = prmt(b4, 0u, j ? 0x4342u : 0x4140u);
-            }
+    {
+      const uint32_t* hb = sH + (vy + R) * WPR + 2 * vq;  // H_k row r: hb[((k-1)*HY + r-vy-R)*WPR]
+      const T* rb = stage + (vy + R) * WBOX + XA2 + 4 * vq;
+      auto term = [&](int k, int dy, int j) -> uint32_t {
+        if (k == 0) {
+          if constexpr (sizeof(T) == 2) {
+            return *reinterpret_cast<const uint32_t*>(rb + dy * WBOX + 2 * j);
+          } else {
+            const uint32_t b4 = *reinterpret_cast<const uint32_t*>(rb + dy * WBOX);
+            return prmt(b4, 0u, j ? 0x4342u : 0x4140u);
           }
-          else t = sH[((k - 1) * HY + r) * WPR + 2 * vq + j];
-          v = op2x2<MAX>(v, t);
         }
-        layer[L][j] = v;
+        return hb[((k - 1) * HY + dy) * WPR + j];
+      };
+#pragma unroll
+      for (int L = 0; L <= R; ++L) {
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          uint32_t v = 0;
+          int nt = 0;
+          uint32_t pend = 0;
+          bool has_pend = false;
+#pragma unroll
+          for (int dy = -R; dy <= R; ++dy) {
+            const int k = S::hw(L, dy);
+            if (k < 0) continue;
+            const uint32_t t = term(k, dy, j);
+            if (nt == 0) {
+              v = t;
+            } else if (!has_pend) {
+              pend = t;
+              has_pend = true;
+            } else {
+              v = op3x2<MAX>(v, pend, t);
+              has_pend = false;
+            }
+            ++nt;
+          }
+          if (has_pend) v = op2x2<MAX>(v, pend);
+          layer[L][j] = v;
+        }
       }
     }
-    // ---- Z: push into the ring; output z = s - 2R completes -------------------
+    // ---- Z: slice s feeds outputs o = s-2R .. s (offset dz = s - o - R, layer
+    // |dz|); output o lives in acc slot o % RING and completes at s = o + 2R
     switch (s % RING) {
 #define HB_M3_CASE(U)                                                                   \
   case U:                                                                               \
     if constexpr (U < RING) {                                                           \
       _Pragma("unroll") for (int d = -R; d <= R; ++d) {                                 \
-        constexpr int dummy = 0; (void)dummy;                                           \
-        const int slot = ((U - d) % RING + RING) % RING;                                \
+        const int slot = ((U - d - R) % RING + RING) % RING; /* o = s - d - R */        \
         const int L = d < 0 ? -d : d;                                                   \
-        acc[slot][0] = op2x2<MAX>(acc[slot][0], layer[L][0]);                           \
-        acc[slot][1] = op2x2<MAX>(acc[slot][1], layer[L][1]);                           \
-      }                                                                                 \
-      {                                                                                 \
-        const int o = s - 2 * R;                                                        \
-        constexpr int slot = ((U - R) % RING + RING) % RING;                            \
-        if (o >= 0) {                                                                   \
-          const int gy = y0 + vy, gx = x0 + 4 * vq;                                     \
-          if (gy < a.ny && gx < a.nx) {                                                 \
-            T* dst = out + ((int64_t)(z0 + o) * a.ny + gy) * (int64_t)a.nx + gx;         \
-            const uint32_t v0 = acc[slot][0], v1 = acc[slot][1];                        \
-            if (gx + 3 < a.nx) {                                                        \
-              if constexpr (sizeof(T) == 2) {                                           \
-                *reinterpret_cast<uint2*>(dst) = make_uint2(v0, v1);                    \
-              } else {                                                                  \
-                *reinterpret_cast<uint32_t*>(dst) = prmt(v0, v1, 0x6420);               \
-              }                                                                         \
-            } else {                                                                    \
-              const uint32_t vv[2] = {v0, v1};                                          \
-              for (int i = 0; i < 4 && gx + i < a.nx; ++i)                              \
-                dst[i] = (T)((vv[i >> 1] >> (16 * (i & 1))) & 0xffffu);                  \
-            }                                                                           \
-          }                                                                             \
+        if (d == R) {                                                                   \
+          const uint32_t v0 = op2x2<MAX>(acc[slot][0], layer[L][0]);                    \
+          const uint32_t v1 = op2x2<MAX>(acc[slot][1], layer[L][1]);                    \
+          if (s >= 2 * R) store_out(s - 2 * R, v0, v1);                                 \
+          acc[slot][0] = acc[slot][1] = IDENT;                                          \
+        } else {                                                                        \
+          acc[slot][0] = op2x2<MAX>(acc[slot][0], layer[L][0]);                         \
+          acc[slot][1] = op2x2<MAX>(acc[slot][1], layer[L][1]);                         \
         }                                                                               \
-        acc[slot][0] = acc[slot][1] = IDENT;                                            \
       }                                                                                 \
     }                                                                                   \
     break;
