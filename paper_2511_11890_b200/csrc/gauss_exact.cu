@@ -124,13 +124,7 @@ k_exact_yx(const __grid_constant__ CUtensorMap tm, float* __restrict__ out, cons
   __syncthreads();
   mbar_wait(bar, 0);
   if ((x0 - R < 0) || (x0 + EY_TX + R > b.nx) || (y0 - R < 0) || (y0 + EY_TY + R > b.ny)) {
-    for (int e = tid; e < G::HB * G::WC; e += EY_NT) {
-      const int ly = e / G::WC, lx = e - ly * G::WC;
-      const int gy = y0 - R + ly, gx = x0 - R + lx;
-      const int cy = min(max(gy, 0), b.ny - 1), cx = min(max(gx, 0), b.nx - 1);
-      if (cy != gy || cx != gx)
-        sIn[ly * G::WBOX + G::XOFF + lx] = sIn[(cy - (y0 - R)) * G::WBOX + G::XOFF + (cx - (x0 - R))];
-    }
+    clamp_tile<float, EY_NT>(sIn + G::XOFF, G::WBOX, G::HB, G::WC, y0 - R, x0 - R, b.ny, b.nx, tid);
     __syncthreads();
   }
   // Y pass: column c, 8 rows per item

@@ -194,15 +194,7 @@ k_sep3d_fused(const __grid_constant__ CUtensorMap tin, const __grid_constant__ C
     mbar_wait(&bar[st], (uint32_t)((s / G::NST) & 1));
     if (border) {
       // clamp-to-edge fix-up of the zero-filled out-of-volume parts
-      for (int e = tid; e < G::HB * G::WC; e += NT) {
-        const int ly = e / G::WC, lx = e - ly * G::WC;
-        const int gy = y0 - R + ly, gx = x0 - R + lx;
-        const int cy = min(max(gy, 0), a.ny - 1), cx = min(max(gx, 0), a.nx - 1);
-        if (cy != gy || cx != gx) {
-          stage[ly * G::WBOX + G::XOFF + lx] =
-              stage[(cy - (y0 - R)) * G::WBOX + G::XOFF + (cx - (x0 - R))];
-        }
-      }
+      clamp_tile<Tin, NT>(stage + G::XOFF, G::WBOX, G::HB, G::WC, y0 - R, x0 - R, a.ny, a.nx, tid);
       fence_proxy_async();  // generic writes before the stage is re-filled by TMA
       __syncthreads();
     }
@@ -560,14 +552,7 @@ k_gauss_p2(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUte
     Tin* stage = sIn + st * (G::STAGE_PITCH / sizeof(Tin));
     mbar_wait(&bar[st], (uint32_t)((s / G::NST) & 1));
     if (border) {
-      for (int e = tid; e < G::HB * G::WC; e += P2_NT) {
-        const int ly = e / G::WC, lx = e - ly * G::WC;
-        const int gy = y0 - R + ly, gx = x0 - R + lx;
-        const int cy = min(max(gy, 0), a.ny - 1), cx = min(max(gx, 0), a.nx - 1);
-        if (cy != gy || cx != gx)
-          stage[ly * G::WBOX + G::XOFF + lx] =
-              stage[(cy - (y0 - R)) * G::WBOX + G::XOFF + (cx - (x0 - R))];
-      }
+      clamp_tile<Tin, P2_NT>(stage + G::XOFF, G::WBOX, G::HB, G::WC, y0 - R, x0 - R, a.ny, a.nx, tid);
       fence_proxy_async();
       __syncthreads();
     }

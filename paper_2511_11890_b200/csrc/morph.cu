@@ -542,38 +542,6 @@ __device__ __forceinline__ uint32_t op3x2(uint32_t a, uint32_t b, uint32_t c) {
   return op2x2<MAX>(op2x2<MAX>(a, b), c);  // ptxas fuses into VIMNMX3.U16x2
 }
 
-// Clamp-to-edge fix-up of a TMA-staged halo'd tile whose out-of-volume parts
-// TMA zero-filled: out-of-range rows are copied whole from the nearest valid
-// row, then out-of-range columns of every row from the nearest valid column.
-// Touches only the halo strips (the per-element loop over the whole tile it
-// replaces was ~20% of k_morph3's instructions at 1024^3).  The caller fences
-// and synchronises afterwards.
-template <typename T, int NT>
-__device__ __forceinline__ void clamp_tile(T* st, int pitch, int h, int w, int gy0, int gx0, int ny,
-                                           int nx, int tid) {
-  const int r_lo = max(0, -gy0), r_hi = min(h, ny - gy0);
-  if (r_lo > 0 || r_hi < h) {
-    const int nbad = r_lo + (h - r_hi);
-    for (int e = tid; e < nbad * w; e += NT) {
-      const int i = e / w, c = e - i * w;
-      const int r = i < r_lo ? i : r_hi + (i - r_lo);
-      const int src = i < r_lo ? r_lo : r_hi - 1;
-      st[r * pitch + c] = st[src * pitch + c];
-    }
-    __syncthreads();
-  }
-  const int c_lo = max(0, -gx0), c_hi = min(w, nx - gx0);
-  if (c_lo > 0 || c_hi < w) {
-    const int nbc = c_lo + (w - c_hi);
-    for (int e = tid; e < h * nbc; e += NT) {
-      const int r = e / nbc, i = e - r * nbc;
-      const int c = i < c_lo ? i : c_hi + (i - c_lo);
-      const int src = i < c_lo ? c_lo : c_hi - 1;
-      st[r * pitch + c] = st[r * pitch + src];
-    }
-  }
-}
-
 template <typename T, bool MAX, int KIND, int R>
 __global__ void __launch_bounds__(M3X_NT, 2)
 k_morph3(const __grid_constant__ CUtensorMap tin, T* __restrict__ out, const Morph3Args a) {
