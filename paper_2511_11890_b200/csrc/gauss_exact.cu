@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <type_traits>
 
 #include "ops.cuh"
 #include "tma.cuh"
@@ -73,6 +74,87 @@ k_exact_z(const T* __restrict__ in, int64_t nz, int64_t plane, int64_t zo, int64
         for (int k = 0; k < W; ++k) win[k] = v[(u + k) % W];
         out[(z - z0 + z0) * plane + col] = fold<R>(win, wv);
         ++z;
+      }
+    }
+  }
+}
+
+// ---- Z pass, TMA-staged (the fast path) ---------------------------------------
+// A CTA owns a 64 x 8 column tile and marches a z-chunk; TMA streams one slice
+// tile per stage through an 8-deep smem ring (loads run 8 slices ahead, so the
+// f64 fold never waits on memory: k_exact_z's one-load-per-step dependency
+// left it latency-bound at 36% FP64 busy).  A thread owns two x-adjacent
+// columns (one LDS.64 per slice) and keeps their (2R+1)-deep f64 windows in
+// registers with static slots (loop unrolled by 2R+1).
+constexpr int Z2_TX = 64, Z2_TY = 8, Z2_NT = 256, Z2_NST = 8;
+
+template <typename T> struct ExTma;
+template <> struct ExTma<float> { static constexpr CUtensorMapDataType v = CU_TENSOR_MAP_DATA_TYPE_FLOAT32; };
+template <> struct ExTma<uint16_t> { static constexpr CUtensorMapDataType v = CU_TENSOR_MAP_DATA_TYPE_UINT16; };
+template <> struct ExTma<uint8_t> { static constexpr CUtensorMapDataType v = CU_TENSOR_MAP_DATA_TYPE_UINT8; };
+
+struct Z2Args {
+  int nz, ny, nx;  // input block
+  int zo, nzo, zchunk;
+};
+
+template <int R, typename T>
+__global__ void __launch_bounds__(Z2_NT, 2)
+k_exact_z2(const __grid_constant__ CUtensorMap tin, float* __restrict__ out, const ExactArgs a,
+           const Z2Args b) {
+  constexpr int W = 2 * R + 1;
+  __shared__ __align__(128) T stg[Z2_NST][Z2_TY][Z2_TX];
+  __shared__ __align__(8) uint64_t bar[Z2_NST];
+  const int tid = threadIdx.x, lane = tid & 31, ty = tid >> 5;
+  const int x0 = blockIdx.x * Z2_TX, y0 = blockIdx.y * Z2_TY;
+  const int zs = blockIdx.z * b.zchunk, ze = min(zs + b.zchunk, b.nzo);
+  const int nsl = ze - zs + 2 * R;
+  auto zin = [&](int i) { return min(max(b.zo + zs - R + i, 0), b.nz - 1); };
+  constexpr uint32_t BYTES = Z2_TX * Z2_TY * sizeof(T);
+  if (tid == 0) {
+    prefetch_tmap(&tin);
+#pragma unroll
+    for (int i = 0; i < Z2_NST; ++i) mbar_init(&bar[i], 1);
+    fence_mbar_init();
+    for (int i = 0; i < Z2_NST && i < nsl; ++i) {
+      mbar_expect_tx(&bar[i], BYTES);
+      tma_load_3d(&stg[i][0][0], &tin, x0, y0, zin(i), &bar[i]);
+    }
+  }
+  __syncthreads();
+  const int gx = x0 + 2 * lane, gy = y0 + ty;
+  const bool ok = gy < b.ny && gx < b.nx;  // nx is even here, so gx + 1 < nx too
+  const int64_t oplane = (int64_t)b.ny * b.nx;
+  float* optr = out + ((int64_t)zs * b.ny + min(gy, b.ny - 1)) * b.nx + min(gx, b.nx - 2);
+  const double* wv = a.w;
+  double v0[W], v1[W];
+  for (int i0 = 0; i0 < nsl; i0 += W) {
+#pragma unroll
+    for (int u = 0; u < W; ++u) {
+      const int i = i0 + u;
+      if (i < nsl) {
+        const int st = i & (Z2_NST - 1);
+        mbar_wait(&bar[st], (uint32_t)((i / Z2_NST) & 1));
+        const T p0 = stg[st][ty][2 * lane], p1 = stg[st][ty][2 * lane + 1];
+        __syncthreads();  // every thread has read stage st
+        if (tid == 0 && i + Z2_NST < nsl) {
+          fence_proxy_async();
+          mbar_expect_tx(&bar[st], BYTES);
+          tma_load_3d(&stg[st][0][0], &tin, x0, y0, zin(i + Z2_NST), &bar[st]);
+        }
+        // slot u holds slice i (i0 is a multiple of W); the reference casts to f32 first
+        v0[u] = (double)(float)p0;
+        v1[u] = (double)(float)p1;
+        if (i >= 2 * R) {
+          double w0[W], w1[W];
+#pragma unroll
+          for (int k = 0; k < W; ++k) {  // window position k = slice i - 2R + k
+            w0[k] = v0[(u + 1 + k) % W];
+            w1[k] = v1[(u + 1 + k) % W];
+          }
+          const float r0 = fold<R>(w0, wv), r1 = fold<R>(w1, wv);
+          if (ok) *reinterpret_cast<float2*>(optr + (int64_t)(i - 2 * R) * oplane) = make_float2(r0, r1);
+        }
       }
     }
   }
@@ -185,8 +267,43 @@ cudaError_t run_exact_r(const DevIn& in, int64_t zo, int64_t nzo, float* out, co
   a.R = R;
   for (int k = 0; k < 2 * R + 1; ++k) a.w[k] = (double)taps.w[k];
   const int64_t plane = in.ny * in.nx;
-  // Z pass -> tmp (nzo slices)
-  {
+  // Z pass -> tmp (nzo slices): TMA-staged kernel when the layout allows it
+  bool z_done = false;
+  if constexpr (sizeof(T) <= 2 || std::is_same<T, float>::value) {
+    CUtensorMap tz;
+    if (make_tmap_3d(&tz, in.p, ExTma<T>::v, sizeof(T), in.nx, in.ny, in.nz, Z2_TX, Z2_TY)) {
+      Z2Args zb;
+      zb.nz = (int)in.nz;
+      zb.ny = (int)in.ny;
+      zb.nx = (int)in.nx;
+      zb.zo = (int)zo;
+      zb.nzo = (int)nzo;
+      const int gx = (int)((in.nx + Z2_TX - 1) / Z2_TX), gy = (int)((in.ny + Z2_TY - 1) / Z2_TY);
+      auto kz = k_exact_z2<R, T>;
+      int per_sm = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kz, Z2_NT, 0) != cudaSuccess || per_sm < 1)
+        per_sm = 1;
+      const int64_t tiles = (int64_t)gx * gy, slots = (int64_t)kNumSMs * per_sm;
+      double best = 1e300;
+      int64_t best_zc = nzo;
+      for (int split = 1; split <= 512; ++split) {
+        const int64_t zc = (nzo + split - 1) / split;
+        if (split > 1 && zc < 8 * R + 8) break;
+        const int64_t ctas = tiles * ((nzo + zc - 1) / zc);
+        const double cost = (double)((ctas + slots - 1) / slots) * (double)(zc + 2 * R);
+        if (cost < best * 0.98) {
+          best = cost;
+          best_zc = zc;
+        }
+      }
+      zb.zchunk = (int)best_zc;
+      dim3 grid(gx, gy, (unsigned)((nzo + best_zc - 1) / best_zc));
+      kz<<<grid, Z2_NT, 0, s>>>(tz, tmp, a, zb);
+      if (launches) *launches += 1;
+      z_done = true;
+    }
+  }
+  if (!z_done) {
     const int64_t cols = (plane + EZ_T - 1) / EZ_T;
     // enough column-chunks in flight to hide the per-step load latency (the
     // window priming costs 2R extra L2 reads per chunk)
