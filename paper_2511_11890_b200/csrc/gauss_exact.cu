@@ -161,7 +161,9 @@ k_exact_z2(const __grid_constant__ CUtensorMap tin, float* __restrict__ out, con
 }
 
 // ---- fused Y + X pass of one slice tile --------------------------------------
-constexpr int EY_TX = 64, EY_TY = 32, EY_NT = 256;
+// 320 threads: the Y pass has (64 + 2R) x 4 = 320 items for R = 8, one per
+// thread (256 threads ran two rounds for 64 of them); the X pass uses 256
+constexpr int EY_TX = 64, EY_TY = 32, EY_NT = 320;
 
 template <int R>
 struct EGeo {
@@ -225,6 +227,7 @@ k_exact_yx(const __grid_constant__ CUtensorMap tm, float* __restrict__ out, cons
   }
   __syncthreads();
   // X pass: row r, 8 outputs per thread
+  if (tid >= 256) return;
   const int r = tid >> 3, xs = (tid & 7) * 8;
   double v[8 + 2 * R];
 #pragma unroll
