@@ -99,30 +99,42 @@ __global__ void __launch_bounds__(32 * W) k_log_stream(const LogArgs a) {
 
   // ring[k] = centre rows of block slice z - 2 + k (k = 0..4); slice z + 3 is
   // loaded a full step ahead into nxt, then the ring rotates by moves.  The y
-  // halo rows of slice z are other warps' centre rows (L1 hits): loaded at the
-  // start of the step and consumed after the z and x terms.
+  // halo rows of slice z (other warps' centre rows: L1/L2 hits) and the strip's
+  // edge columns are loaded a step ahead as well.
   float4 ring[5][RY];
   const int64_t zb0 = a.zo + oz0;
 #pragma unroll
   for (int k = 0; k < 5; ++k) load_centre(zb0 - 2 + k, ring[k]);
   float* dst = a.out + (int64_t)oz0 * plane + (int64_t)y0 * nx + xl;
+  auto load_halo = [&](int64_t zb, float4 (&h)[4], float (&e)[RY][2]) {
+    const float* p = slice(zb);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) h[k] = __ldg(reinterpret_cast<const float4*>(p + hrow[k] + xc));
+    if (edge_lane) {
+#pragma unroll
+      for (int r = 0; r < RY; ++r) {
+        e[r][0] = __ldg(p + crow[r] + e0);
+        e[r][1] = __ldg(p + crow[r] + e1);
+      }
+    }
+  };
+  float4 hal_n[4];
+  float el_n[RY][2] = {};
+  load_halo(zb0, hal_n, el_n);
 
 #pragma unroll 1
   for (int o = oz0; o < oz1; ++o) {
     const int64_t z = a.zo + o;
     float4 nxt[RY];
-    if (o + 1 < oz1) load_centre(z + 3, nxt);
-    const float* pz = slice(z);
     float4 hal[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) hal[k] = __ldg(reinterpret_cast<const float4*>(pz + hrow[k] + xc));
     float el[RY][2];
-    if (edge_lane) {
 #pragma unroll
-      for (int r = 0; r < RY; ++r) {
-        el[r][0] = __ldg(pz + crow[r] + e0);
-        el[r][1] = __ldg(pz + crow[r] + e1);
-      }
+    for (int k = 0; k < 4; ++k) hal[k] = hal_n[k];
+#pragma unroll
+    for (int r = 0; r < RY; ++r) el[r][0] = el_n[r][0], el[r][1] = el_n[r][1];
+    if (o + 1 < oz1) {
+      load_centre(z + 3, nxt);
+      load_halo(z + 1, hal_n, el_n);  // the next step's halo, a step ahead
     }
     const bool z_face = z < 2 || z > nz - 3;
     float res[RY][4];
