@@ -36,11 +36,12 @@ METRICS = [
 ]
 
 KEYS = {"k_median3_plane": "median", "k_box_stream": "mean", "k_gauss_p2<8": "gaussian",
-        "k_morph3": "erode", "k_log_stream": "log_stage2", "k_exact_z<8": "exact_z",
+        "k_morph3": "erode", "k_log_stream": "log_stage2", "k_exact_z2<8": "exact_z",
         "k_exact_yx<8": "exact_yx"}
 
 
 def main(rep, out_md):
+    """rep: one report or several joined with ','"""
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                          text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
