@@ -288,8 +288,10 @@ k_median3_plane(const T* __restrict__ in, int64_t nz, int64_t ny, int64_t nx, in
   const int tid = threadIdx.x;
   const int tx = tid & 31, ty = tid >> 5;
   const int64_t x0 = (int64_t)blockIdx.x * M3_TX, y0 = (int64_t)blockIdx.y * M3_TY;
-  const int64_t zs = (int64_t)blockIdx.z * zchunk;
-  const int64_t ze = min(zs + (int64_t)zchunk, nzo);
+  // 32-bit z bookkeeping (slices < 2^30): 64-bit compares/selects in the step
+  // loop cost ~10 uniform-datapath issue slots per output
+  const int zs = (int)blockIdx.z * zchunk;
+  const int ze = min(zs + zchunk, (int)nzo);
   // cooperative slice loader: element e of the halo'd tile -> (ly, lx)
   constexpr int NE = M3_H * M3_W;
   constexpr int PER = (NE + 255) / 256;
@@ -307,7 +309,8 @@ k_median3_plane(const T* __restrict__ in, int64_t nz, int64_t ny, int64_t nx, in
   // fetch keeps the raw samples; the key conversion happens in stash, one
   // step later, so the global-load latency overlaps a whole step of sorting.
   // Slices are addressed by a running pointer (clamped only at the volume faces).
-  auto slice_ptr = [&](int64_t zb) { return in + clamp64(zb, 0, nz - 1) * plane; };
+  const int zlast = (int)nz - 1;
+  auto slice_ptr = [&](int zb) { return in + (int64_t)min(max(zb, 0), zlast) * plane; };
   auto fetch = [&](const T* src, T (&v)[PER]) {
 #pragma unroll
     for (int k = 0; k < PER; ++k) v[k] = gval[k] ? __ldg(src + goff[k]) : T(0);
@@ -330,7 +333,7 @@ k_median3_plane(const T* __restrict__ in, int64_t nz, int64_t ny, int64_t nx, in
   };
   const int64_t gy = y0 + ty, gx = x0 + 2 * tx;
   const bool st_y = gy < ny, st_x0 = gx < nx, st_x1 = gx + 1 < nx;
-  T* optr = out + (zs) * plane + gy * nx + gx;  // output slice zs, advanced per step
+  T* optr = out + (int64_t)zs * plane + gy * nx + gx;  // output slice zs, advanced per step
   auto emit = [&](int k0, int k1) {
     if (st_y) {
       if (st_x0) optr[0] = from_key<T>(k0);
@@ -347,22 +350,26 @@ k_median3_plane(const T* __restrict__ in, int64_t nz, int64_t ny, int64_t nx, in
   // it was read, so one barrier per step orders all reads before the rewrite
   int* const tb0 = &tile[0][0][0];
   constexpr int TPITCH = M3_H * M3_W;
-  fetch(slice_ptr(zo + zs - 1), v);
+  const int zb0 = (int)zo + zs;
+  fetch(slice_ptr(zb0 - 1), v);
   stash(tb0, v);
-  fetch(slice_ptr(zo + zs), v);
+  fetch(slice_ptr(zb0), v);
   stash(tb0 + TPITCH, v);
-  // next slice to fetch: block z = zo + zs + 1, then + 1 per step (clamped at faces)
-  int64_t zf = zo + zs + 1;
-  fetch(slice_ptr(zf), v);
+  // next slice to fetch: block z = zb0 + 1, then + 1 per step; a running
+  // pointer that stops advancing at the last slice (the clamp at the face)
+  int zf = zb0 + 1;
+  const T* pf = slice_ptr(zf);
+  fetch(pf, v);
   __syncthreads();
   planes(tb0, X[0], X[1]);           // P(zs-1)
   planes(tb0 + TPITCH, Y[0], Y[1]);  // P(zs)
-  int64_t z = zs;
+  int z = zs;
   int* tb = tb0 + 2 * TPITCH;  // buffer that receives slice z+1
   auto next_plane = [&](int (&pa)[9], int (&pb)[9]) {
     stash(tb, v);
     ++zf;
-    fetch(slice_ptr(zf), v);
+    if (zf <= zlast && zf > 0) pf += plane;
+    fetch(pf, v);
     __syncthreads();
     planes(tb, pa, pb);
     tb = (tb == tb0 + 2 * TPITCH) ? tb0 : tb + TPITCH;
