@@ -79,3 +79,12 @@ def test_host_helpers(golden):
     assert L.hb_chain_out_dtype(mp.arr, mp.n, _native.HB_U16) == _native.HB_U16
     bad = _native._Marshalled(_native.DeviceProgram([_native.Stage(_native.OP_MEDIAN, radius=0)]))
     assert L.hb_chain_halo(bad.arr, bad.n) == -1
+
+
+def test_session_and_pinned_are_public_api():
+    """session()/pinned() are exported and bind to the declared C symbols."""
+    import paper_2511_11890_b200 as hb
+    from paper_2511_11890_b200 import _native
+
+    assert callable(hb.session) and callable(hb.pinned)
+    assert "hb_session_begin" in _native.EXPORTS and "hb_session_end" in _native.EXPORTS
