@@ -464,6 +464,7 @@ template <> __device__ __forceinline__ f2 load_pair<float>(const float* p) {
 
 struct P2Args {
   unsigned long long w2[kMaxTaps > 17 ? 17 : kMaxTaps];  // (w_k, w_k) pairs
+  float w1[kMaxTaps > 17 ? 17 : kMaxTaps];               // w_k (FFMA constant operands)
   int nzi, zo, nzo, zchunk, nx, ny;
   const void* orig;
   float amount;
@@ -489,15 +490,19 @@ struct GeoP2 {
   static constexpr int NST = 3;
   static constexpr int RING = 2 * R + 1;
   static constexpr int NYI = NYP * (P2_TY / P2_YR);            // Y-pass items
-  static constexpr int P2 = NYC + 4;                           // sY row-pair pitch (f2)
-  static constexpr int SY_BYTES = 2 * (P2_TY / 2) * P2 * 8;
+  // X pass: R >= 6 reads 4 x positions of a row from a row-major sY in scalar
+  // FP32 (halves the X pass's shared-memory bytes, the bottleneck at large R);
+  // smaller R keep the FFMA2 row-pair X pass on a row-pair interleaved sY
+  static constexpr bool XQ = R >= 6;
+  static constexpr int SYP = NYC + 4;                          // sY pitch (floats / f2)
+  static constexpr int SY_BYTES = XQ ? 2 * P2_TY * SYP * 4 : 2 * (P2_TY / 2) * SYP * 8;
   static constexpr int SOUT_BYTES = 3 * P2_TY * P2_TX * 4;     // triple-buffered
   static constexpr int OFF_SY = NST * STAGE_PITCH;
   static constexpr int OFF_SOUT = OFF_SY + SY_BYTES;
   static constexpr int OFF_BAR = OFF_SOUT + SOUT_BYTES;
   static constexpr int SMEM = OFF_BAR + NST * 8 + 128;
   static_assert(NYI <= P2_NT, "Y-pass items exceed the CTA");
-  static_assert((P2_TY / 2) * (P2_TX / 2) == P2_NT, "one thread per (row pair, x pair)");
+  static_assert(P2_TY * (P2_TX / 4) == P2_NT, "one thread per (row, 4 x) / (row pair, 2 x)");
 };
 
 template <int R, typename Tin, bool UNSHARP, int P2_YR>
@@ -510,7 +515,7 @@ k_gauss_p2(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUte
   unsigned char* smem =
       smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u)  /* stays in .shared */;
   Tin* sIn = reinterpret_cast<Tin*>(smem);
-  f2* sY = reinterpret_cast<f2*>(smem + G::OFF_SY);
+  float* sY = reinterpret_cast<float*>(smem + G::OFF_SY);
   float* sOut = reinterpret_cast<float*>(smem + G::OFF_SOUT);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + G::OFF_BAR);
   const int tid = threadIdx.x;
@@ -541,7 +546,9 @@ k_gauss_p2(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUte
   // Y item: column pair ycp, rows [P2_YR * yg, P2_YR * yg + P2_YR)
   const int ycp = tid % G::NYP, yg = tid / G::NYP;
   const bool y_active = tid < G::NYI;
-  // X/Z ownership: row pair yp, x positions 2*sg, 2*sg+1
+  // X/Z ownership: XQ: row yr, x positions 4*xq .. 4*xq+3 (ring of two x pairs);
+  // otherwise row pair yp, x positions 2*sg, 2*sg+1 (ring of two row pairs)
+  const int yr = tid / (P2_TX / 4), xq = tid % (P2_TX / 4);
   const int yp = tid / (P2_TX / 2), sg = tid % (P2_TX / 2);
   f2 ring[G::RING][2];
 #pragma unroll
@@ -556,8 +563,8 @@ k_gauss_p2(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUte
       fence_proxy_async();
       __syncthreads();
     }
-    // ---- Y pass (column pairs, scatter form) -> sY row-pair interleaved ------
-    f2* sYb = sY + (s & 1) * (P2_TY / 2) * G::P2;
+    // ---- Y pass (column pairs, scatter form) -> sY --------------------------
+    float* sYb = sY + (s & 1) * P2_TY * G::SYP;  // same float count in both layouts
     if (y_active) {
       f2 acc[P2_YR];
       const Tin* src = stage + (P2_YR * yg) * G::WBOX + G::YC0 + 2 * ycp;
@@ -571,17 +578,24 @@ k_gauss_p2(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUte
           else if (k > 0 && k <= 2 * R) acc[m] = fma(v, W[k], acc[m]);
         }
       }
+      if constexpr (G::XQ) {
 #pragma unroll
-      for (int m = 0; m < P2_YR; m += 2) {
-        float a0, a1, b0, b1;
-        upk(acc[m], a0, a1);      // row m:   (c, c+1)
-        upk(acc[m + 1], b0, b1);  // row m+1: (c, c+1)
-        uint4 q;
-        q.x = __float_as_uint(a0);
-        q.y = __float_as_uint(b0);
-        q.z = __float_as_uint(a1);
-        q.w = __float_as_uint(b1);
-        *reinterpret_cast<uint4*>(sYb + ((P2_YR * yg + m) / 2) * G::P2 + 2 * ycp) = q;
+        for (int m = 0; m < P2_YR; ++m)  // row m: columns (c, c+1), one STS.64
+          *reinterpret_cast<f2*>(sYb + (P2_YR * yg + m) * G::SYP + 2 * ycp) = acc[m];
+      } else {
+        f2* sYp = reinterpret_cast<f2*>(sYb);
+#pragma unroll
+        for (int m = 0; m < P2_YR; m += 2) {  // row pair: [(c,r0),(c,r1)],[(c+1,r0),(c+1,r1)]
+          float a0, a1, b0, b1;
+          upk(acc[m], a0, a1);
+          upk(acc[m + 1], b0, b1);
+          uint4 q;
+          q.x = __float_as_uint(a0);
+          q.y = __float_as_uint(b0);
+          q.z = __float_as_uint(a1);
+          q.w = __float_as_uint(b1);
+          *reinterpret_cast<uint4*>(sYp + ((P2_YR * yg + m) / 2) * G::SYP + 2 * ycp) = q;
+        }
       }
     }
     __syncthreads();
@@ -598,11 +612,44 @@ k_gauss_p2(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUte
         bulk_wait_read<1>();
       }
     }
-    // ---- X pass (row pairs, scatter form), written straight into the ring slot
-    // two partial sums per output (taps <= R / > R) halve the dependent chain
-    auto xpass = [&](f2& out0, f2& out1) {
+    // ---- X pass: 4 x positions of one row in scalar FP32 (the shifted taps of
+    // x-adjacent outputs do not form aligned register pairs), 20 floats in
+    // five LDS.128 -> half the shared-memory bytes of a row-pair X pass, which
+    // kept the LSU pipe 71% busy; results land straight in the ring slot as
+    // two x pairs.  Two partial sums per output halve the dependent chain.
+    auto xpass_q = [&](f2& out0, f2& out1) {
+      float xa[4], xb[4];
+      const float* row = sYb + yr * G::SYP + G::YOFF + 4 * xq;
+      auto tap = [&](int c, float v) {
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          const int k = c - m;
+          const float wk = a.w1[k < 0 ? 0 : (k > 2 * R ? 0 : k)];
+          if (k == 0) xa[m] = v * wk;
+          else if (k == R + 1) xb[m] = v * wk;
+          else if (k > 0 && k <= R) xa[m] = fmaf(v, wk, xa[m]);
+          else if (k > R + 1 && k <= 2 * R) xb[m] = fmaf(v, wk, xb[m]);
+        }
+      };
+      if (G::YOFF == 0) {
+#pragma unroll
+        for (int i = 0; i < (4 + 2 * R + 3) / 4; ++i) {
+          const float4 q = *reinterpret_cast<const float4*>(row + 4 * i);
+          tap(4 * i, q.x);
+          tap(4 * i + 1, q.y);
+          tap(4 * i + 2, q.z);
+          tap(4 * i + 3, q.w);
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < 4 + 2 * R; ++c) tap(c, row[c]);
+      }
+      out0 = pk(xa[0] + xb[0], xa[1] + xb[1]);
+      out1 = pk(xa[2] + xb[2], xa[3] + xb[3]);
+    };
+    auto xpass_rp = [&](f2& out0, f2& out1) {  // row-pair FFMA2 X pass (small R)
       f2 xa[2], xb[2];
-      const f2* row = sYb + yp * G::P2 + G::YOFF + 2 * sg;
+      const f2* row = reinterpret_cast<const f2*>(sYb) + yp * G::SYP + G::YOFF + 2 * sg;
       auto tap = [&](int c, f2 v) {
 #pragma unroll
         for (int m = 0; m < 2; ++m) {
@@ -629,6 +676,10 @@ k_gauss_p2(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUte
       }
       out0 = add(xa[0], xb[0]);
       out1 = add(xa[1], xb[1]);
+    };
+    auto xpass = [&](f2& out0, f2& out1) {
+      if constexpr (G::XQ) xpass_q(out0, out1);
+      else xpass_rp(out0, out1);
     };
     // ---- ring + Z pass (symmetric fold) --------------------------------------
     const int o = s - 2 * R;
@@ -658,27 +709,32 @@ k_gauss_p2(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUte
       default: break;
     }
     if (have) {
-      float r0[2], r1[2];  // rows 2yp, 2yp+1 at x = 2sg, 2sg+1
-      upk(zr[0], r0[0], r1[0]);
-      upk(zr[1], r0[1], r1[1]);
+      float r[4];  // XQ: row yr at x = 4xq..4xq+3; else rows 2yp (r0, r1), 2yp+1 (r2, r3) at x 2sg, 2sg+1
+      if constexpr (G::XQ) {
+        upk(zr[0], r[0], r[1]);
+        upk(zr[1], r[2], r[3]);
+      } else {
+        upk(zr[0], r[0], r[2]);
+        upk(zr[1], r[1], r[3]);
+      }
       if (UNSHARP) {
         const int64_t zb = (int64_t)a.zo + z0 + o;
         const Tin* ob = reinterpret_cast<const Tin*>(a.orig);
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int gy = min(y0 + 2 * yp + h, a.ny - 1);
-          const Tin* orow = ob + (zb * a.ny + gy) * (int64_t)a.nx;
-          float* rr = h ? r1 : r0;
-#pragma unroll
-          for (int m = 0; m < 2; ++m) {
-            const float b = (float)__ldg(orow + min(x0 + 2 * sg + m, a.nx - 1));
-            rr[m] = __fadd_rn(b, __fmul_rn(a.amount, __fsub_rn(b, rr[m])));
-          }
+        for (int m = 0; m < 4; ++m) {
+          const int gy = G::XQ ? y0 + yr : y0 + 2 * yp + (m >> 1);
+          const int gx = G::XQ ? x0 + 4 * xq + m : x0 + 2 * sg + (m & 1);
+          const float b = (float)__ldg(ob + (zb * a.ny + min(gy, a.ny - 1)) * (int64_t)a.nx + min(gx, a.nx - 1));
+          r[m] = __fadd_rn(b, __fmul_rn(a.amount, __fsub_rn(b, r[m])));
         }
       }
-      float* dst = sOut + (o % 3) * P2_TY * P2_TX + (2 * yp) * P2_TX + 2 * sg;
-      *reinterpret_cast<float2*>(dst) = make_float2(r0[0], r0[1]);
-      *reinterpret_cast<float2*>(dst + P2_TX) = make_float2(r1[0], r1[1]);
+      float* tile = sOut + (o % 3) * P2_TY * P2_TX;
+      if constexpr (G::XQ) {
+        *reinterpret_cast<float4*>(tile + yr * P2_TX + 4 * xq) = make_float4(r[0], r[1], r[2], r[3]);
+      } else {
+        *reinterpret_cast<float2*>(tile + (2 * yp) * P2_TX + 2 * sg) = make_float2(r[0], r[1]);
+        *reinterpret_cast<float2*>(tile + (2 * yp + 1) * P2_TX + 2 * sg) = make_float2(r[2], r[3]);
+      }
       fence_proxy_async();
     }
   }
@@ -707,6 +763,7 @@ cudaError_t launch_p2(const DevIn& in, int64_t zo, int64_t nzo, float* out, cons
     unsigned int b = 0;
     std::memcpy(&b, &taps.w[k], 4);
     a.w2[k] = ((unsigned long long)b << 32) | b;
+    a.w1[k] = taps.w[k];
   }
   a.nzi = (int)in.nz;
   a.zo = (int)zo;
