@@ -320,3 +320,15 @@ def test_device_session_keeps_pool_until_exit(hb):
         assert _native.device_pool_bytes() > 0
     assert _native.device_pool_bytes() == 0
     assert np.array_equal(a, registry.run_operator(x, "median", {"radius": 1})[0])
+
+
+def test_bench_harness_runs_on_device(hb):
+    """harpia/bench.py's run_bench over the device executor: one row per ladder
+    entry, zero residual device memory, sane throughput."""
+    from paper_2511_11890_b200 import bench
+
+    sc = bench.BenchScenario(op="median", params={"radius": 1}, ladder=(16, 32), base_yx=64,
+                             repeats=3, dtype="float32")
+    rows = bench.run_bench(sc)
+    assert [r.size_bytes for r in rows] == [16 * 64 * 64 * 4, 32 * 64 * 64 * 4]
+    assert all(r.device_residual_bytes == 0 and r.residual_bytes == 0 and r.gvox_s > 0 for r in rows)

@@ -251,3 +251,31 @@ def test_ledger_semantics():
     assert L.snapshot().residual_bytes == 0
     with pytest.raises(ValueError):
         L.charge(-1)
+
+
+def test_bench_module_mirrors_reference(tmp_path):
+    """paper_2511_11890_b200.bench mirrors harpia/bench.py: seeded synthetic
+    volumes (bench.py:63-68), scenario validation (bench.py:46-51) and the CSV
+    header (bench.py:25)."""
+    import numpy as np
+    import pytest
+
+    from paper_2511_11890_b200 import bench
+    from paper_2511_11890_b200.errors import ParameterError
+
+    v = bench.synthesize(3, 5, "uint16", 7)
+    assert v.dtype == np.uint16 and v.shape == (3, 5, 5)
+    assert np.array_equal(v, np.random.default_rng(7).integers(0, 65536, size=(3, 5, 5), dtype="uint16"))
+    f = bench.synthesize(2, 4, "float32", 0)
+    assert np.array_equal(f, np.random.default_rng(0).random((2, 4, 4), dtype=np.float32))
+    assert bench.CSV_HEADER == ("size_bytes", "mean_s", "std_s", "peak_bytes", "residual_bytes")
+    with pytest.raises(ParameterError):
+        bench.BenchScenario(op="median", repeats=0)
+    with pytest.raises(ParameterError):
+        bench.BenchScenario(op="median", ladder=(64, 64))
+    rows = [bench.BenchRow(10, 0.5, 0.1, 7, 0, 1.25, 99, 0, 10, 10)]
+    p = tmp_path / "b.csv"
+    bench.write_csv(rows, p)
+    assert p.read_text().splitlines() == ["size_bytes,mean_s,std_s,peak_bytes,residual_bytes", "10,0.5,0.1,7,0"]
+    bench.write_csv(rows, p, device_columns=True)
+    assert p.read_text().splitlines()[0].endswith("gvox_s,device_peak_bytes,device_residual_bytes,h2d_bytes,d2h_bytes")
