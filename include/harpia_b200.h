@@ -70,8 +70,14 @@ typedef enum {
   HB_OP_UNSHARP = 4,  /* filters.py:136-139  */
   HB_OP_LOG = 5,      /* hessian trace, filters.py:234-264 */
   HB_OP_ERODE = 6,    /* morphology.py:114-116 */
-  HB_OP_DILATE = 7    /* morphology.py:119-121 (caller passes the SE; the
+  HB_OP_DILATE = 7,   /* morphology.py:119-121 (caller passes the SE; the
                          library reflects it, as the reference does) */
+  /* SURVEY.md §8(f) row 2, the next local map ops on the same machinery: */
+  HB_OP_HESSIAN = 8,  /* one component, filters.py:246-253; radius = component
+                         index 0..5 = xx, yy, zz, xy, xz, yz (filters.py:228) */
+  HB_OP_SOBEL = 9,    /* filters.py:200-202 */
+  HB_OP_PREWITT = 10, /* filters.py:205-207 */
+  HB_OP_THRESHOLD = 11 /* threshold.py:110-112; amount = t; uint32 labels */
 } hb_op;
 
 typedef enum {
@@ -83,10 +89,10 @@ typedef enum {
  * expressed as chains of erode/dilate stages (morphology.py:124-140). */
 typedef struct {
   int32_t op;          /* hb_op */
-  int32_t precision;   /* hb_precision (gaussian/unsharp/log) */
-  double sigma;        /* gaussian/unsharp/log */
-  double amount;       /* unsharp */
-  int32_t radius;      /* mean/median */
+  int32_t precision;   /* hb_precision (gaussian/unsharp/log/hessian) */
+  double sigma;        /* gaussian/unsharp/log/hessian */
+  double amount;       /* unsharp: amount; threshold: t */
+  int32_t radius;      /* mean/median: radius; hessian: component index */
   int32_t n_offsets;   /* erode/dilate: number of (dz,dy,dx) triples */
   const int32_t* offsets; /* erode/dilate: 3*n_offsets ints, must contain origin */
   int32_t n_weights;   /* gaussian/unsharp/log: 2*ceil(4 sigma)+1, or 0 */

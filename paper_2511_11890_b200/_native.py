@@ -25,6 +25,7 @@ LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libharpia_b200.so"
 HB_U8, HB_U16, HB_U32, HB_F32 = 0, 1, 2, 3
 HB_HOST, HB_DEVICE = 0, 1
 OP_IDENTITY, OP_GAUSSIAN, OP_MEAN, OP_MEDIAN, OP_UNSHARP, OP_LOG, OP_ERODE, OP_DILATE = range(8)
+OP_HESSIAN, OP_SOBEL, OP_PREWITT, OP_THRESHOLD = range(8, 12)
 PREC_FAST, PREC_EXACT = 0, 1
 
 DTYPE_CODE = {
@@ -207,8 +208,10 @@ class Stage:
     def halo(self) -> int:
         if self.op in (OP_GAUSSIAN, OP_UNSHARP):
             return (len(self.weights) - 1) // 2
-        if self.op == OP_LOG:
+        if self.op in (OP_LOG, OP_HESSIAN):
             return (len(self.weights) - 1) // 2 + 2
+        if self.op in (OP_SOBEL, OP_PREWITT):
+            return 1
         if self.op in (OP_MEAN, OP_MEDIAN):
             return int(self.radius)
         if self.op in (OP_ERODE, OP_DILATE):
@@ -216,8 +219,10 @@ class Stage:
         return 0
 
     def out_dtype(self, in_dtype: np.dtype) -> np.dtype:
-        if self.op in (OP_GAUSSIAN, OP_UNSHARP, OP_LOG, OP_MEAN):
+        if self.op in (OP_GAUSSIAN, OP_UNSHARP, OP_LOG, OP_MEAN, OP_HESSIAN, OP_SOBEL, OP_PREWITT):
             return np.dtype("float32")
+        if self.op == OP_THRESHOLD:
+            return np.dtype("uint32")  # LABEL_DTYPE (volume.py:23)
         return np.dtype(in_dtype)
 
 

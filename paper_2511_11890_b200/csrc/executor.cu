@@ -46,6 +46,7 @@ struct StageDesc {
   float amount = 0.f;
   Taps taps{};
   std::vector<int32_t> offsets;  // reflected for dilation
+  double threshold = 0.0;        // apply_threshold's t (kept in f64, NumPy semantics)
   int in_dt = HB_F32, out_dt = HB_F32;
 };
 
@@ -107,7 +108,8 @@ hb_status normalise(const hb_stage* st, int nst, int in_dt, std::vector<StageDes
         break;
       case HB_OP_GAUSSIAN:
       case HB_OP_UNSHARP:
-      case HB_OP_LOG: {
+      case HB_OP_LOG:
+      case HB_OP_HESSIAN: {
         if (!(s.sigma > 0) || !std::isfinite(s.sigma)) {
           msg = "sigma must be positive, got " + std::to_string(s.sigma);
           return HB_EPARAM;
@@ -132,12 +134,27 @@ hb_status normalise(const hb_stage* st, int nst, int in_dt, std::vector<StageDes
             msg = "gaussian weights must be symmetric";
             return HB_EPARAM;
           }
-        d.halo = r + (s.op == HB_OP_LOG ? 2 : 0);
+        d.halo = r + (s.op == HB_OP_LOG || s.op == HB_OP_HESSIAN ? 2 : 0);
         d.amount = (float)s.amount;
-        if (s.op == HB_OP_LOG) d.precision = s.precision;  // exact recommended
+        if (s.op == HB_OP_HESSIAN) {
+          if (s.radius < 0 || s.radius > 5) {
+            msg = "hessian component index must be 0..5 (xx, yy, zz, xy, xz, yz)";
+            return HB_EPARAM;
+          }
+          d.radius = s.radius;
+        }
         d.out_dt = HB_F32;
         break;
       }
+      case HB_OP_SOBEL:
+      case HB_OP_PREWITT:
+        d.halo = 1;
+        d.out_dt = HB_F32;
+        break;
+      case HB_OP_THRESHOLD:
+        d.threshold = s.amount;  // NaN compares false everywhere, as in NumPy
+        d.out_dt = HB_U32;
+        break;
       case HB_OP_MEAN:
       case HB_OP_MEDIAN:
         if (s.radius < 1) {
@@ -282,7 +299,7 @@ size_t chain_scratch(const std::vector<StageDesc>& st, int64_t nz, int64_t ny, i
     // per-op temporaries (generic gaussian: one f32 buffer; LoG: g + tmp)
     if (st[s].op == HB_OP_GAUSSIAN || st[s].op == HB_OP_UNSHARP || st[s].op == HB_OP_MEAN)
       total += n * plane * 4;
-    if (st[s].op == HB_OP_LOG) {
+    if (st[s].op == HB_OP_LOG || st[s].op == HB_OP_HESSIAN) {
       int64_t in_n = s == 0 ? nz : (rg[s - 1].b - rg[s - 1].a);
       size_t gn = (size_t)std::min<int64_t>(in_n, n + 4);
       total += 2 * gn * plane * 4;
@@ -336,7 +353,13 @@ cudaError_t run_stage(const StageDesc& d, const DevIn& in, int64_t zo, int64_t n
       if (!tmp) return pa.err;
       return mean_generic(in, zo, nzo, (float*)out, d.radius, tmp, s, launches);
     }
-    case HB_OP_LOG: {
+    case HB_OP_SOBEL:
+    case HB_OP_PREWITT:
+      return gradmag(in, zo, nzo, (float*)out, d.op == HB_OP_SOBEL, s, launches);
+    case HB_OP_THRESHOLD:
+      return threshold(in, zo, nzo, (uint32_t*)out, d.threshold, s, launches);
+    case HB_OP_LOG:
+    case HB_OP_HESSIAN: {
       // smoothed g over [zo-2, zo+nzo+2) ∩ [0, nz) then the cd∘cd stage
       int64_t g0 = std::max<int64_t>(0, zo - 2), g1 = std::min<int64_t>(in.nz, zo + nzo + 2);
       float* g = (float*)pa.get((size_t)(g1 - g0) * plane * 4);
@@ -358,6 +381,12 @@ cudaError_t run_stage(const StageDesc& d, const DevIn& in, int64_t zo, int64_t n
         }
       }
       if (e != cudaSuccess) return e;
+      if (d.op == HB_OP_HESSIAN) {
+        // component index -> (a, b) axes, x = 2, y = 1, z = 0 (filters.py:228-231)
+        static const int ax[6][2] = {{2, 2}, {1, 1}, {0, 0}, {2, 1}, {2, 0}, {1, 0}};
+        return hessian_stage(g, g0, in.nz, in.ny, in.nx, zo, nzo, ax[d.radius][0],
+                             ax[d.radius][1], (float*)out, s, launches);
+      }
       return log_diff(g, g0, g1 - g0, in.nz, in.ny, in.nx, zo, nzo, (float*)out, s, launches);
     }
     case HB_OP_MEDIAN:

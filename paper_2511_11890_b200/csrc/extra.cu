@@ -1,0 +1,174 @@
+// extra.cu — the next local map operators on the same chunk machinery
+// (SURVEY.md §8(f) row 2): single Hessian components, Sobel / Prewitt gradient
+// magnitude and apply_threshold.  All three are bit-exact restatements:
+//   hessian_ab = cd_b(cd_a(g)), cd(f)[i] = 0.5 * (f[clamp(i+1)] - f[clamp(i-1)])
+//       in float32 on the exact Gaussian g (filters.py:246-253);
+//   sobel / prewitt: per derivative axis, three 3-tap correlate1d passes
+//       (z, y, x; f64 accumulation in NI_Correlate1D's symmetric /
+//       antisymmetric fold, f32 rounding per pass), total += comp*comp in f32,
+//       sqrt (filters.py:187-207);
+//   apply_threshold: data > t as uint32 labels with NumPy 2 comparison
+//       semantics (float32 data compares against float32(t), integer data in
+//       float64) (threshold.py:110-112).
+// These are memory-/latency-light per-voxel kernels (one thread per output,
+// x fastest, neighbours through L1): not on the benchmarked path.
+#include <cuda_runtime.h>
+
+#include <type_traits>
+
+#include "ops.cuh"
+
+namespace hb {
+namespace {
+
+constexpr int kT = 256;
+
+inline int grid_for(int64_t n) {
+  int64_t b = (n + kT - 1) / kT;
+  const int64_t cap = (int64_t)kNumSMs * 32;
+  return (int)(b < 1 ? 1 : (b < cap ? b : cap));
+}
+
+__global__ void __launch_bounds__(kT)
+k_hessian_comp(const float* __restrict__ g, int64_t gz0, int nz, int ny, int nx, int64_t zo,
+               int64_t nzo, int axis_a, int axis_b, float* __restrict__ out) {
+  const int64_t plane = (int64_t)ny * nx, total = nzo * plane;
+  const int n[3] = {nz, ny, nx};
+  for (int64_t i = blockIdx.x * (int64_t)kT + threadIdx.x; i < total; i += (int64_t)gridDim.x * kT) {
+    const int64_t zl = i / plane;
+    const int64_t rr = i - zl * plane;
+    int p[3] = {(int)(zo + zl), (int)(rr / nx), (int)(rr % nx)};
+    auto at = [&](const int (&q)[3]) {
+      return __ldg(g + ((int64_t)(q[0] - gz0) * ny + q[1]) * nx + q[2]);
+    };
+    // inner cd along a at position q (clamped per step)
+    auto cd_a = [&](int (&q)[3]) {
+      const int c = q[axis_a];
+      q[axis_a] = min(c + 1, n[axis_a] - 1);
+      const float hi = at(q);
+      q[axis_a] = max(c - 1, 0);
+      const float lo = at(q);
+      q[axis_a] = c;
+      return __fmul_rn(0.5f, __fsub_rn(hi, lo));
+    };
+    const int c = p[axis_b];
+    p[axis_b] = min(c + 1, n[axis_b] - 1);
+    const float dp = cd_a(p);
+    p[axis_b] = max(c - 1, 0);
+    const float dm = cd_a(p);
+    out[i] = __fmul_rn(0.5f, __fsub_rn(dp, dm));
+  }
+}
+
+// one 3-tap correlate1d output, NI_Correlate1D fold order, f64, rounded to f32
+__device__ __forceinline__ float corr3(float xm, float x0, float xp, double w0, double w1, int sym) {
+  const double m = (double)xm, c = (double)x0, p = (double)xp;
+  double acc = __dmul_rn(c, w1);
+  if (sym > 0) acc = __dadd_rn(acc, __dmul_rn(__dadd_rn(m, p), w0));
+  else acc = __dadd_rn(acc, __dmul_rn(__dsub_rn(m, p), w0));
+  return (float)acc;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kT)
+k_gradmag(const T* __restrict__ in, int nz, int ny, int nx, int64_t zo, int64_t nzo,
+          float smooth_mid, float* __restrict__ out) {
+  const int64_t plane = (int64_t)ny * nx, total = nzo * plane;
+  for (int64_t i = blockIdx.x * (int64_t)kT + threadIdx.x; i < total; i += (int64_t)gridDim.x * kT) {
+    const int64_t zl = i / plane;
+    const int64_t rr = i - zl * plane;
+    const int z = (int)(zo + zl), y = (int)(rr / nx), x = (int)(rr % nx);
+    // the clamped 3x3x3 window (each separable pass clamps along its own axis,
+    // which is the same as clamping the window once)
+    float v[3][3][3];
+#pragma unroll
+    for (int dz = 0; dz < 3; ++dz) {
+      const int zc = min(max(z + dz - 1, 0), nz - 1);
+#pragma unroll
+      for (int dy = 0; dy < 3; ++dy) {
+        const int yc = min(max(y + dy - 1, 0), ny - 1);
+        const T* row = in + ((int64_t)zc * ny + yc) * nx;
+#pragma unroll
+        for (int dx = 0; dx < 3; ++dx) v[dz][dy][dx] = (float)__ldg(row + min(max(x + dx - 1, 0), nx - 1));
+      }
+    }
+    float total_sq = 0.f;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      // weights (w0 = outer, w1 = centre): deriv [-1, 0, 1] is antisymmetric
+      // with w0 = -1; smoothing [1, m, 1] is symmetric with w0 = 1
+      const double w0z = d == 0 ? -1.0 : 1.0, w1z = d == 0 ? 0.0 : (double)smooth_mid;
+      const double w0y = d == 1 ? -1.0 : 1.0, w1y = d == 1 ? 0.0 : (double)smooth_mid;
+      const double w0x = d == 2 ? -1.0 : 1.0, w1x = d == 2 ? 0.0 : (double)smooth_mid;
+      const int sz = d == 0 ? -1 : 1, sy = d == 1 ? -1 : 1, sx = d == 2 ? -1 : 1;
+      float a[3][3];  // z pass at the 3x3 (y, x) positions
+#pragma unroll
+      for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+        for (int dx = 0; dx < 3; ++dx) a[dy][dx] = corr3(v[0][dy][dx], v[1][dy][dx], v[2][dy][dx], w0z, w1z, sz);
+      float b[3];  // y pass at the 3 x positions
+#pragma unroll
+      for (int dx = 0; dx < 3; ++dx) b[dx] = corr3(a[0][dx], a[1][dx], a[2][dx], w0y, w1y, sy);
+      const float comp = corr3(b[0], b[1], b[2], w0x, w1x, sx);
+      total_sq = __fadd_rn(total_sq, __fmul_rn(comp, comp));
+    }
+    out[i] = __fsqrt_rn(total_sq);
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kT)
+k_threshold(const T* __restrict__ in, int64_t n, double t, uint32_t* __restrict__ out) {
+  const float tf = (float)t;
+  for (int64_t i = blockIdx.x * (int64_t)kT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kT) {
+    const T v = __ldg(in + i);
+    if constexpr (std::is_same<T, float>::value) out[i] = v > tf ? 1u : 0u;
+    else out[i] = (double)v > t ? 1u : 0u;
+  }
+}
+
+}  // namespace
+
+cudaError_t hessian_stage(const float* g, int64_t gz0, int64_t nz, int64_t ny, int64_t nx,
+                          int64_t zo, int64_t nzo, int axis_a, int axis_b, float* out,
+                          cudaStream_t s, int64_t* launches) {
+  if (nzo <= 0) return cudaSuccess;
+  k_hessian_comp<<<grid_for(nzo * ny * nx), kT, 0, s>>>(g, gz0, (int)nz, (int)ny, (int)nx, zo, nzo,
+                                                         axis_a, axis_b, out);
+  if (launches) *launches += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t gradmag(const DevIn& in, int64_t zo, int64_t nzo, float* out, bool sobel,
+                    cudaStream_t s, int64_t* launches) {
+  if (nzo <= 0) return cudaSuccess;
+  const float mid = sobel ? 2.f : 1.f;
+  const int g = grid_for(nzo * in.ny * in.nx);
+  switch (in.dt) {
+    case HB_U8: k_gradmag<uint8_t><<<g, kT, 0, s>>>((const uint8_t*)in.p, (int)in.nz, (int)in.ny, (int)in.nx, zo, nzo, mid, out); break;
+    case HB_U16: k_gradmag<uint16_t><<<g, kT, 0, s>>>((const uint16_t*)in.p, (int)in.nz, (int)in.ny, (int)in.nx, zo, nzo, mid, out); break;
+    case HB_U32: k_gradmag<uint32_t><<<g, kT, 0, s>>>((const uint32_t*)in.p, (int)in.nz, (int)in.ny, (int)in.nx, zo, nzo, mid, out); break;
+    case HB_F32: k_gradmag<float><<<g, kT, 0, s>>>((const float*)in.p, (int)in.nz, (int)in.ny, (int)in.nx, zo, nzo, mid, out); break;
+    default: return cudaErrorInvalidValue;
+  }
+  if (launches) *launches += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t threshold(const DevIn& in, int64_t zo, int64_t nzo, uint32_t* out, double t,
+                      cudaStream_t s, int64_t* launches) {
+  if (nzo <= 0) return cudaSuccess;
+  const int64_t plane = in.ny * in.nx, n = nzo * plane;
+  const int g = grid_for(n);
+  switch (in.dt) {
+    case HB_U8: k_threshold<uint8_t><<<g, kT, 0, s>>>((const uint8_t*)in.p + zo * plane, n, t, out); break;
+    case HB_U16: k_threshold<uint16_t><<<g, kT, 0, s>>>((const uint16_t*)in.p + zo * plane, n, t, out); break;
+    case HB_U32: k_threshold<uint32_t><<<g, kT, 0, s>>>((const uint32_t*)in.p + zo * plane, n, t, out); break;
+    case HB_F32: k_threshold<float><<<g, kT, 0, s>>>((const float*)in.p + zo * plane, n, t, out); break;
+    default: return cudaErrorInvalidValue;
+  }
+  if (launches) *launches += 1;
+  return cudaGetLastError();
+}
+
+}  // namespace hb

@@ -58,6 +58,16 @@ cudaError_t log_diff(const float* g, int64_t gz0, int64_t ngz, int64_t nz, int64
 cudaError_t log_diff_stream(const float* g, int64_t gz0, int64_t nz, int64_t ny, int64_t nx,
                             int64_t zo, int64_t nzo, float* out, cudaStream_t s,
                             int64_t* launches);
+// next local map ops (extra.cu): one Hessian component cd_b(cd_a(g)) of a
+// smoothed block g laid out like log_diff's; Sobel/Prewitt gradient
+// magnitude; apply_threshold -> uint32 labels
+cudaError_t hessian_stage(const float* g, int64_t gz0, int64_t nz, int64_t ny, int64_t nx,
+                          int64_t zo, int64_t nzo, int axis_a, int axis_b, float* out,
+                          cudaStream_t s, int64_t* launches);
+cudaError_t gradmag(const DevIn& in, int64_t zo, int64_t nzo, float* out, bool sobel,
+                    cudaStream_t s, int64_t* launches);
+cudaError_t threshold(const DevIn& in, int64_t zo, int64_t nzo, uint32_t* out, double t,
+                      cudaStream_t s, int64_t* launches);
 // dtype conversion / copy (identity op, registry.py:127-133)
 cudaError_t copy_slices(const DevIn& in, int64_t zo, int64_t nzo, void* out,
                         cudaStream_t s, int64_t* launches);

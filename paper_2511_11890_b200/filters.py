@@ -96,6 +96,30 @@ def log_program(sigma, precision="exact") -> _native.DeviceProgram:
         weights=_gaussian_kernel(sigma))])
 
 
+HESSIAN_COMPONENTS = ("xx", "yy", "zz", "xy", "xz", "yz")  # filters.py:228
+
+
+def hessian_program(sigma, component, precision="exact") -> _native.DeviceProgram:
+    _check_sigma(sigma)
+    if component not in HESSIAN_COMPONENTS:
+        raise ParameterError(f"component must be one of {HESSIAN_COMPONENTS}, got {component!r}")
+    return _native.DeviceProgram([_native.Stage(
+        _native.OP_HESSIAN, precision=_precision(precision), sigma=float(sigma),
+        radius=HESSIAN_COMPONENTS.index(component), weights=_gaussian_kernel(sigma))])
+
+
+def sobel_program() -> _native.DeviceProgram:
+    return _native.DeviceProgram([_native.Stage(_native.OP_SOBEL)])
+
+
+def prewitt_program() -> _native.DeviceProgram:
+    return _native.DeviceProgram([_native.Stage(_native.OP_PREWITT)])
+
+
+def threshold_program(t) -> _native.DeviceProgram:
+    return _native.DeviceProgram([_native.Stage(_native.OP_THRESHOLD, amount=float(t))])
+
+
 def identity_program() -> _native.DeviceProgram:
     return _native.DeviceProgram([_native.Stage(_native.OP_IDENTITY)])
 
@@ -202,3 +226,24 @@ def unsharp(data, sigma, amount, precision="fast"):
 def log(data, sigma, precision="exact"):
     """Laplacian of Gaussian = hessian_xx + hessian_yy + hessian_zz (filters.py:246-264)."""
     return apply_program(data, log_program(sigma, precision))
+
+
+def hessian_component(data, sigma, component, precision="exact"):
+    """One second-derivative component cd_b(cd_a(gaussian(data, sigma)))
+    (filters.py:246-253); bit-exact with the default exact smoothing."""
+    return apply_program(data, hessian_program(sigma, component, precision))
+
+
+def hessian(data, sigma, precision="exact"):
+    """All six Hessian components (filters.py:256-264)."""
+    return {c: hessian_component(data, sigma, c, precision) for c in HESSIAN_COMPONENTS}
+
+
+def sobel(data):
+    """3D gradient magnitude with [1,2,1] cross-axis smoothing (filters.py:200-202)."""
+    return apply_program(data, sobel_program())
+
+
+def prewitt(data):
+    """3D gradient magnitude with [1,1,1] cross-axis smoothing (filters.py:205-207)."""
+    return apply_program(data, prewitt_program())

@@ -26,6 +26,7 @@ from .errors import ParameterError
 
 REQUIRED = object()
 FLOAT32 = np.dtype("float32")
+LABEL_DTYPE = np.dtype("uint32")  # volume.py:23
 
 
 @dataclass(frozen=True)
@@ -164,8 +165,8 @@ def _direct(program_of):
     return lambda b, p, a: filters.apply_program(b, program_of(p))
 
 
-def _map(name, schema, profile, program_of):
-    register(Operator(name=name, kind="map", output="volume", schema=schema, profile=profile,
+def _map(name, schema, profile, program_of, output="volume"):
+    register(Operator(name=name, kind="map", output=output, schema=schema, profile=profile,
                       fn=_direct(program_of), program=program_of))
 
 
@@ -192,6 +193,23 @@ _map("unsharp",
      lambda p: OpProfile(halo_z=filters.gaussian_kernel_radius(p["sigma"]), scratch_factor=10,
                          out_dtype=FLOAT32),
      lambda p: filters.unsharp_program(p["sigma"], p["amount"], p["precision"]))
+
+# hessian_* (registry.py:234-246), sobel / prewitt
+# (registry.py:210-224), apply_threshold (registry.py:248-255) on the device
+for _comp in filters.HESSIAN_COMPONENTS:
+    _map(f"hessian_{_comp}",
+         {"sigma": (float, REQUIRED), "precision": (_precision_param, "exact")},
+         lambda p: OpProfile(halo_z=filters.gaussian_kernel_radius(p["sigma"]) + 2,
+                             scratch_factor=10, out_dtype=FLOAT32),
+         (lambda comp: lambda p: filters.hessian_program(p["sigma"], comp, p["precision"]))(_comp))
+
+_map("sobel", {}, lambda p: OpProfile(halo_z=1, scratch_factor=12, out_dtype=FLOAT32),
+     lambda p: filters.sobel_program())
+_map("prewitt", {}, lambda p: OpProfile(halo_z=1, scratch_factor=12, out_dtype=FLOAT32),
+     lambda p: filters.prewitt_program())
+_map("apply_threshold", {"t": (float, REQUIRED)},
+     lambda p: OpProfile(halo_z=0, scratch_factor=6, out_dtype=LABEL_DTYPE),
+     lambda p: filters.threshold_program(p["t"]), output="labels")
 
 # LoG = hessian trace; profile as the reference's hessian_* (registry.py:234-246)
 _map("log",

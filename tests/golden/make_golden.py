@@ -76,6 +76,20 @@ def main():
         h = F.hessian(vols[vol], 1.5)
         add(f"log_{vol}", "log", {"sigma": 1.5}, vol, (h["xx"] + h["yy"]) + h["zz"])
     add("median_u8_r3", "median", {"radius": 3}, "u8_a", F.median(vols["u8_a"], 3))
+    # the next local map ops on the same machinery
+    T = ref.threshold
+    for vol in ("f32_a", "f32_neg", "u8_a", "f32_col", "f32_thin"):
+        for comp in F.HESSIAN_COMPONENTS:
+            add(f"hessian_{comp}_{vol}", f"hessian_{comp}", {"sigma": 1.5}, vol,
+                F.hessian_component(vols[vol], 1.5, comp))
+    for vol in ("f32_a", "f32_unit", "f32_thin", "f32_col", "u8_a", "u16_a", "f32_neg"):
+        add(f"sobel_{vol}", "sobel", {}, vol, F.sobel(vols[vol]))
+        add(f"prewitt_{vol}", "prewitt", {}, vol, F.prewitt(vols[vol]))
+    for vol, ts in (("f32_unit", (0.1, 0.5)), ("u8_a", (127.5, 3.0)), ("u16_a", (30000.25,)),
+                    ("f32_neg", (0.0, -12.3))):
+        for t in ts:
+            add(f"apply_threshold_{vol}_{t}", "apply_threshold", {"t": t}, vol,
+                T.apply_threshold(vols[vol], t))
     for vol in ("u8_a", "u16_a", "bin_a", "f32_neg"):
         for se in ("ball:1", "ball:2", "ball:3", "box:1", "cross:2"):
             s = M.StructuringElement.parse(se)
@@ -114,7 +128,8 @@ def main():
                          ("median", {"radius": 2}), ("unsharp", {"sigma": 1.0, "amount": 1.5}),
                          ("hessian_xx", {"sigma": 2.0}), ("morph_erode", {"se": "ball:3"}),
                          ("morph_open", {"se": "ball:3", "iterations": 2}),
-                         ("identity", {})]:
+                         ("identity", {}), ("hessian_xy", {"sigma": 1.5}), ("sobel", {}),
+                         ("prewitt", {}), ("apply_threshold", {"t": 0.5})]:
         op = R.get_operator(name)
         pr = op.profile(R.validate_params(op, params))
         profiles[name] = {"params": params, "halo_z": pr.halo_z, "scratch": pr.scratch_factor,

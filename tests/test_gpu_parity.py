@@ -116,6 +116,11 @@ ALL_OPS = [
     ("morph_dilate", {"se": "box:1"}, "u8"),
     ("morph_open", {"se": "ball:1", "iterations": 2}, "bin"),
     ("morph_close", {"se": "cross:1"}, "u8"),
+    ("hessian_xz", {"sigma": 1.5}, "f32"),
+    ("hessian_yy", {"sigma": 1.0}, "u16"),
+    ("sobel", {}, "u8"),
+    ("prewitt", {}, "f32"),
+    ("apply_threshold", {"t": 0.5}, "f32"),
 ]
 
 
@@ -332,3 +337,22 @@ def test_bench_harness_runs_on_device(hb):
     rows = bench.run_bench(sc)
     assert [r.size_bytes for r in rows] == [16 * 64 * 64 * 4, 32 * 64 * 64 * 4]
     assert all(r.device_residual_bytes == 0 and r.residual_bytes == 0 and r.gvox_s > 0 for r in rows)
+
+
+@pytest.mark.parametrize("shape", [(21, 37, 132), (9, 1, 40), (6, 33, 7)])
+def test_next_map_ops_vs_oracle(hb, oracle, shape):
+    """SURVEY.md §8(f) row 2 ops (hessian components, sobel, prewitt,
+    apply_threshold): bit-exact against the oracle on ragged shapes."""
+    from paper_2511_11890_b200 import filters, threshold
+
+    rng = np.random.default_rng(sum(shape) + 7)
+    for dt in ("f32", "u16", "u8"):
+        x = _vol(rng, shape, dt)
+        for comp in filters.HESSIAN_COMPONENTS:
+            assert np.array_equal(filters.hessian_component(x, 1.2, comp),
+                                  oracle.hessian_component(x, 1.2, comp)), (dt, comp)
+        assert np.array_equal(filters.sobel(x), oracle.sobel(x)), dt
+        assert np.array_equal(filters.prewitt(x), oracle.prewitt(x)), dt
+        t = 0.37 if dt == "f32" else 100.5
+        got = threshold.apply_threshold(x, t)
+        assert got.dtype == np.uint32 and np.array_equal(got, oracle.apply_threshold(x, t)), dt

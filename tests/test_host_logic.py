@@ -78,12 +78,15 @@ class TestRegistry:
     def test_names(self):
         assert set(registry.operator_names()) == {
             "identity", "gaussian", "mean", "median", "unsharp", "log",
-            "morph_erode", "morph_dilate", "morph_open", "morph_close"}
+            "morph_erode", "morph_dilate", "morph_open", "morph_close",
+            # SURVEY.md §8(f) row 2
+            "hessian_xx", "hessian_yy", "hessian_zz", "hessian_xy", "hessian_xz", "hessian_yz",
+            "sobel", "prewitt", "apply_threshold"}
 
     def test_profiles_match_reference(self, golden):
         meta, _ = golden
         for name, want in meta["profiles"].items():
-            ours = "log" if name == "hessian_xx" else name
+            ours = name
             op = registry.get_operator(ours)
             pr = op.profile(registry.validate_params(op, want["params"]))
             assert pr.halo_z == want["halo_z"], name
