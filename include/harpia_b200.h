@@ -77,7 +77,8 @@ typedef enum {
                          index 0..5 = xx, yy, zz, xy, xz, yz (filters.py:228) */
   HB_OP_SOBEL = 9,    /* filters.py:200-202 */
   HB_OP_PREWITT = 10, /* filters.py:205-207 */
-  HB_OP_THRESHOLD = 11 /* threshold.py:110-112; amount = t; uint32 labels */
+  HB_OP_THRESHOLD = 11, /* threshold.py:110-112; amount = t; uint32 labels */
+  HB_OP_LBP2D = 12    /* filters.py:213-227; uint8 per-slice codes */
 } hb_op;
 
 typedef enum {

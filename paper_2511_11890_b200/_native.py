@@ -25,7 +25,7 @@ LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libharpia_b200.so"
 HB_U8, HB_U16, HB_U32, HB_F32 = 0, 1, 2, 3
 HB_HOST, HB_DEVICE = 0, 1
 OP_IDENTITY, OP_GAUSSIAN, OP_MEAN, OP_MEDIAN, OP_UNSHARP, OP_LOG, OP_ERODE, OP_DILATE = range(8)
-OP_HESSIAN, OP_SOBEL, OP_PREWITT, OP_THRESHOLD = range(8, 12)
+OP_HESSIAN, OP_SOBEL, OP_PREWITT, OP_THRESHOLD, OP_LBP2D = range(8, 13)
 PREC_FAST, PREC_EXACT = 0, 1
 
 DTYPE_CODE = {
@@ -223,6 +223,8 @@ class Stage:
             return np.dtype("float32")
         if self.op == OP_THRESHOLD:
             return np.dtype("uint32")  # LABEL_DTYPE (volume.py:23)
+        if self.op == OP_LBP2D:
+            return np.dtype("uint8")
         return np.dtype(in_dtype)
 
 

@@ -155,6 +155,9 @@ hb_status normalise(const hb_stage* st, int nst, int in_dt, std::vector<StageDes
         d.threshold = s.amount;  // NaN compares false everywhere, as in NumPy
         d.out_dt = HB_U32;
         break;
+      case HB_OP_LBP2D:
+        d.out_dt = HB_U8;
+        break;
       case HB_OP_MEAN:
       case HB_OP_MEDIAN:
         if (s.radius < 1) {
@@ -358,6 +361,8 @@ cudaError_t run_stage(const StageDesc& d, const DevIn& in, int64_t zo, int64_t n
       return gradmag(in, zo, nzo, (float*)out, d.op == HB_OP_SOBEL, s, launches);
     case HB_OP_THRESHOLD:
       return threshold(in, zo, nzo, (uint32_t*)out, d.threshold, s, launches);
+    case HB_OP_LBP2D:
+      return lbp2d(in, zo, nzo, (uint8_t*)out, s, launches);
     case HB_OP_LOG:
     case HB_OP_HESSIAN: {
       // smoothed g over [zo-2, zo+nzo+2) ∩ [0, nz) then the cd∘cd stage

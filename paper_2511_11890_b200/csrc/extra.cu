@@ -127,7 +127,45 @@ k_threshold(const T* __restrict__ in, int64_t n, double t, uint32_t* __restrict_
   }
 }
 
+// lbp2d: bit (7 - k) set when neighbour k >= centre, neighbours clockwise from
+// the top-left, edge-clamped in y/x; comparisons in the input dtype
+template <typename T>
+__global__ void __launch_bounds__(kT)
+k_lbp2d(const T* __restrict__ in, int ny, int nx, int64_t n, uint8_t* __restrict__ out) {
+  const int64_t plane = (int64_t)ny * nx;
+  for (int64_t i = blockIdx.x * (int64_t)kT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kT) {
+    const int64_t zl = i / plane;
+    const int64_t rr = i - zl * plane;
+    const int y = (int)(rr / nx), x = (int)(rr % nx);
+    const T* sl = in + zl * plane;
+    const T c = __ldg(sl + rr);
+    const int ym = max(y - 1, 0) * nx, y0 = y * nx, yp = min(y + 1, ny - 1) * nx;
+    const int xm = max(x - 1, 0), xp = min(x + 1, nx - 1);
+    const int nb[8] = {ym + xm, ym + x, ym + xp, y0 + xp, yp + xp, yp + x, yp + xm, y0 + xm};
+    uint32_t b = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) b |= (__ldg(sl + nb[k]) >= c ? 1u : 0u) << (7 - k);
+    out[i] = (uint8_t)b;
+  }
+}
+
 }  // namespace
+
+cudaError_t lbp2d(const DevIn& in, int64_t zo, int64_t nzo, uint8_t* out, cudaStream_t s,
+                  int64_t* launches) {
+  if (nzo <= 0) return cudaSuccess;
+  const int64_t plane = in.ny * in.nx, n = nzo * plane;
+  const int g = grid_for(n);
+  switch (in.dt) {
+    case HB_U8: k_lbp2d<uint8_t><<<g, kT, 0, s>>>((const uint8_t*)in.p + zo * plane, (int)in.ny, (int)in.nx, n, out); break;
+    case HB_U16: k_lbp2d<uint16_t><<<g, kT, 0, s>>>((const uint16_t*)in.p + zo * plane, (int)in.ny, (int)in.nx, n, out); break;
+    case HB_U32: k_lbp2d<uint32_t><<<g, kT, 0, s>>>((const uint32_t*)in.p + zo * plane, (int)in.ny, (int)in.nx, n, out); break;
+    case HB_F32: k_lbp2d<float><<<g, kT, 0, s>>>((const float*)in.p + zo * plane, (int)in.ny, (int)in.nx, n, out); break;
+    default: return cudaErrorInvalidValue;
+  }
+  if (launches) *launches += 1;
+  return cudaGetLastError();
+}
 
 cudaError_t hessian_stage(const float* g, int64_t gz0, int64_t nz, int64_t ny, int64_t nx,
                           int64_t zo, int64_t nzo, int axis_a, int axis_b, float* out,

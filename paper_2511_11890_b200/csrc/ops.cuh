@@ -68,6 +68,8 @@ cudaError_t gradmag(const DevIn& in, int64_t zo, int64_t nzo, float* out, bool s
                     cudaStream_t s, int64_t* launches);
 cudaError_t threshold(const DevIn& in, int64_t zo, int64_t nzo, uint32_t* out, double t,
                       cudaStream_t s, int64_t* launches);
+cudaError_t lbp2d(const DevIn& in, int64_t zo, int64_t nzo, uint8_t* out, cudaStream_t s,
+                  int64_t* launches);
 // dtype conversion / copy (identity op, registry.py:127-133)
 cudaError_t copy_slices(const DevIn& in, int64_t zo, int64_t nzo, void* out,
                         cudaStream_t s, int64_t* launches);

@@ -116,6 +116,10 @@ def prewitt_program() -> _native.DeviceProgram:
     return _native.DeviceProgram([_native.Stage(_native.OP_PREWITT)])
 
 
+def lbp2d_program() -> _native.DeviceProgram:
+    return _native.DeviceProgram([_native.Stage(_native.OP_LBP2D)])
+
+
 def threshold_program(t) -> _native.DeviceProgram:
     return _native.DeviceProgram([_native.Stage(_native.OP_THRESHOLD, amount=float(t))])
 
@@ -242,6 +246,11 @@ def hessian(data, sigma, precision="exact"):
 def sobel(data):
     """3D gradient magnitude with [1,2,1] cross-axis smoothing (filters.py:200-202)."""
     return apply_program(data, sobel_program())
+
+
+def lbp2d(data):
+    """Per-Z-slice 8-neighbour local binary pattern, uint8 (filters.py:213-227)."""
+    return apply_program(data, lbp2d_program())
 
 
 def prewitt(data):

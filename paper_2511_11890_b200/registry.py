@@ -207,6 +207,8 @@ _map("sobel", {}, lambda p: OpProfile(halo_z=1, scratch_factor=12, out_dtype=FLO
      lambda p: filters.sobel_program())
 _map("prewitt", {}, lambda p: OpProfile(halo_z=1, scratch_factor=12, out_dtype=FLOAT32),
      lambda p: filters.prewitt_program())
+_map("lbp2d", {}, lambda p: OpProfile(halo_z=0, scratch_factor=4, out_dtype=np.dtype("uint8")),
+     lambda p: filters.lbp2d_program())
 _map("apply_threshold", {"t": (float, REQUIRED)},
      lambda p: OpProfile(halo_z=0, scratch_factor=6, out_dtype=LABEL_DTYPE),
      lambda p: filters.threshold_program(p["t"]), output="labels")

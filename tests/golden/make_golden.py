@@ -85,6 +85,8 @@ def main():
     for vol in ("f32_a", "f32_unit", "f32_thin", "f32_col", "u8_a", "u16_a", "f32_neg"):
         add(f"sobel_{vol}", "sobel", {}, vol, F.sobel(vols[vol]))
         add(f"prewitt_{vol}", "prewitt", {}, vol, F.prewitt(vols[vol]))
+    for vol in ("f32_a", "f32_thin", "f32_col", "u8_a", "u16_a", "bin_a", "f32_neg"):
+        add(f"lbp2d_{vol}", "lbp2d", {}, vol, F.lbp2d(vols[vol]))
     for vol, ts in (("f32_unit", (0.1, 0.5)), ("u8_a", (127.5, 3.0)), ("u16_a", (30000.25,)),
                     ("f32_neg", (0.0, -12.3))):
         for t in ts:
@@ -129,7 +131,7 @@ def main():
                          ("hessian_xx", {"sigma": 2.0}), ("morph_erode", {"se": "ball:3"}),
                          ("morph_open", {"se": "ball:3", "iterations": 2}),
                          ("identity", {}), ("hessian_xy", {"sigma": 1.5}), ("sobel", {}),
-                         ("prewitt", {}), ("apply_threshold", {"t": 0.5})]:
+                         ("prewitt", {}), ("apply_threshold", {"t": 0.5}), ("lbp2d", {})]:
         op = R.get_operator(name)
         pr = op.profile(R.validate_params(op, params))
         profiles[name] = {"params": params, "halo_z": pr.halo_z, "scratch": pr.scratch_factor,

@@ -354,5 +354,6 @@ def test_next_map_ops_vs_oracle(hb, oracle, shape):
         assert np.array_equal(filters.sobel(x), oracle.sobel(x)), dt
         assert np.array_equal(filters.prewitt(x), oracle.prewitt(x)), dt
         t = 0.37 if dt == "f32" else 100.5
+        assert np.array_equal(filters.lbp2d(x), oracle.lbp2d(x)), dt
         got = threshold.apply_threshold(x, t)
         assert got.dtype == np.uint32 and np.array_equal(got, oracle.apply_threshold(x, t)), dt
