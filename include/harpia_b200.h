@@ -78,7 +78,10 @@ typedef enum {
   HB_OP_SOBEL = 9,    /* filters.py:200-202 */
   HB_OP_PREWITT = 10, /* filters.py:205-207 */
   HB_OP_THRESHOLD = 11, /* threshold.py:110-112; amount = t; uint32 labels */
-  HB_OP_LBP2D = 12    /* filters.py:213-227; uint8 per-slice codes */
+  HB_OP_LBP2D = 12,   /* filters.py:213-227; uint8 per-slice codes */
+  HB_OP_DIFFUSION = 13 /* anisotropic_diffusion, filters.py:142-184: radius =
+                          iterations, sigma = kappa, amount = dt, precision =
+                          mode (0 exponential, 1 rational) */
 } hb_op;
 
 typedef enum {

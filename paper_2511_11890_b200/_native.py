@@ -25,7 +25,7 @@ LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libharpia_b200.so"
 HB_U8, HB_U16, HB_U32, HB_F32 = 0, 1, 2, 3
 HB_HOST, HB_DEVICE = 0, 1
 OP_IDENTITY, OP_GAUSSIAN, OP_MEAN, OP_MEDIAN, OP_UNSHARP, OP_LOG, OP_ERODE, OP_DILATE = range(8)
-OP_HESSIAN, OP_SOBEL, OP_PREWITT, OP_THRESHOLD, OP_LBP2D = range(8, 13)
+OP_HESSIAN, OP_SOBEL, OP_PREWITT, OP_THRESHOLD, OP_LBP2D, OP_DIFFUSION = range(8, 14)
 PREC_FAST, PREC_EXACT = 0, 1
 
 DTYPE_CODE = {
@@ -212,6 +212,8 @@ class Stage:
             return (len(self.weights) - 1) // 2 + 2
         if self.op in (OP_SOBEL, OP_PREWITT):
             return 1
+        if self.op == OP_DIFFUSION:
+            return int(self.radius)
         if self.op in (OP_MEAN, OP_MEDIAN):
             return int(self.radius)
         if self.op in (OP_ERODE, OP_DILATE):
@@ -219,7 +221,8 @@ class Stage:
         return 0
 
     def out_dtype(self, in_dtype: np.dtype) -> np.dtype:
-        if self.op in (OP_GAUSSIAN, OP_UNSHARP, OP_LOG, OP_MEAN, OP_HESSIAN, OP_SOBEL, OP_PREWITT):
+        if self.op in (OP_GAUSSIAN, OP_UNSHARP, OP_LOG, OP_MEAN, OP_HESSIAN, OP_SOBEL, OP_PREWITT,
+                       OP_DIFFUSION):
             return np.dtype("float32")
         if self.op == OP_THRESHOLD:
             return np.dtype("uint32")  # LABEL_DTYPE (volume.py:23)

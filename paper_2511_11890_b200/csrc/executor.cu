@@ -47,6 +47,7 @@ struct StageDesc {
   Taps taps{};
   std::vector<int32_t> offsets;  // reflected for dilation
   double threshold = 0.0;        // apply_threshold's t (kept in f64, NumPy semantics)
+  float kappa = 0.f;             // anisotropic diffusion
   int in_dt = HB_F32, out_dt = HB_F32;
 };
 
@@ -157,6 +158,26 @@ hb_status normalise(const hb_stage* st, int nst, int in_dt, std::vector<StageDes
         break;
       case HB_OP_LBP2D:
         d.out_dt = HB_U8;
+        break;
+      case HB_OP_DIFFUSION:  // filters.py:152-159 validation
+        if (s.radius < 1) {
+          msg = "iterations must be >= 1, got " + std::to_string(s.radius);
+          return HB_EPARAM;
+        }
+        if (!(s.amount > 0) || s.amount > 1.0 / 6.0 + 1e-12) {
+          msg = "dt must be in (0, 1/6], got " + std::to_string(s.amount);
+          return HB_EPARAM;
+        }
+        if (!(s.sigma > 0)) {
+          msg = "kappa must be positive, got " + std::to_string(s.sigma);
+          return HB_EPARAM;
+        }
+        d.radius = s.radius;
+        d.halo = s.radius;  // each explicit step widens the stencil by one slice
+        d.kappa = (float)s.sigma;
+        d.amount = (float)s.amount;
+        d.precision = s.precision;
+        d.out_dt = HB_F32;
         break;
       case HB_OP_MEAN:
       case HB_OP_MEDIAN:
@@ -302,6 +323,10 @@ size_t chain_scratch(const std::vector<StageDesc>& st, int64_t nz, int64_t ny, i
     // per-op temporaries (generic gaussian: one f32 buffer; LoG: g + tmp)
     if (st[s].op == HB_OP_GAUSSIAN || st[s].op == HB_OP_UNSHARP || st[s].op == HB_OP_MEAN)
       total += n * plane * 4;
+    if (st[s].op == HB_OP_DIFFUSION) {
+      int64_t in_n = s == 0 ? nz : (rg[s - 1].b - rg[s - 1].a);
+      total += 2 * (size_t)in_n * plane * 4;
+    }
     if (st[s].op == HB_OP_LOG || st[s].op == HB_OP_HESSIAN) {
       int64_t in_n = s == 0 ? nz : (rg[s - 1].b - rg[s - 1].a);
       size_t gn = (size_t)std::min<int64_t>(in_n, n + 4);
@@ -363,6 +388,13 @@ cudaError_t run_stage(const StageDesc& d, const DevIn& in, int64_t zo, int64_t n
       return threshold(in, zo, nzo, (uint32_t*)out, d.threshold, s, launches);
     case HB_OP_LBP2D:
       return lbp2d(in, zo, nzo, (uint8_t*)out, s, launches);
+    case HB_OP_DIFFUSION: {
+      float* b0 = (float*)pa.get((size_t)in.nz * plane * 4);
+      float* b1 = (float*)pa.get((size_t)in.nz * plane * 4);
+      if (!b0 || !b1) return pa.err;
+      return diffusion(in, zo, nzo, (float*)out, d.radius, d.kappa, d.amount,
+                       d.precision == 1, b0, b1, s, launches);
+    }
     case HB_OP_LOG:
     case HB_OP_HESSIAN: {
       // smoothed g over [zo-2, zo+nzo+2) ∩ [0, nz) then the cd∘cd stage

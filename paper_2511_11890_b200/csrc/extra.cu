@@ -149,7 +149,74 @@ k_lbp2d(const T* __restrict__ in, int ny, int nx, int64_t n, uint8_t* __restrict
   }
 }
 
+template <typename T>
+__global__ void __launch_bounds__(kT) k_to_f32(const T* __restrict__ in, int64_t n, float* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)kT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kT)
+    out[i] = (float)__ldg(in + i);
+}
+
+// one Perona-Malik step over the 6 axial neighbours (filters.py:166-183), the
+// reference's float32 op order: per axis t = g(fwd)*fwd + g(bwd)*bwd, flux += t
+// (flux starts at +0), out = c + dt*flux; fwd = 0 past the last slice of the
+// block, bwd = -(c - prev) and 0 at the first
+__device__ __forceinline__ float diff_g(float v, float kappa, bool rational) {
+  const float sc = __fdiv_rn(v, kappa);
+  const float s2 = __fmul_rn(sc, sc);
+  return rational ? __fdiv_rn(1.0f, __fadd_rn(1.0f, s2)) : expf(-s2);
+}
+
+__global__ void __launch_bounds__(kT)
+k_diffusion_step(const float* __restrict__ src, float* __restrict__ dst, int nz, int ny, int nx,
+                 float kappa, float dt, bool rational) {
+  const int64_t plane = (int64_t)ny * nx, n = (int64_t)nz * plane;
+  for (int64_t i = blockIdx.x * (int64_t)kT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kT) {
+    const int z = (int)(i / plane);
+    const int64_t rr = i - (int64_t)z * plane;
+    const int y = (int)(rr / nx), x = (int)(rr % nx);
+    const float c = src[i];
+    const int crd[3] = {z, y, x}, ext[3] = {nz, ny, nx};
+    const int64_t str[3] = {plane, nx, 1};
+    float flux = 0.0f;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const float fwd = crd[a] < ext[a] - 1 ? __fsub_rn(src[i + str[a]], c) : 0.0f;
+      const float bwd = crd[a] > 0 ? -__fsub_rn(c, src[i - str[a]]) : 0.0f;
+      const float t = __fadd_rn(__fmul_rn(diff_g(fwd, kappa, rational), fwd),
+                                __fmul_rn(diff_g(bwd, kappa, rational), bwd));
+      flux = __fadd_rn(flux, t);
+    }
+    dst[i] = __fadd_rn(c, __fmul_rn(dt, flux));
+  }
+}
+
 }  // namespace
+
+cudaError_t diffusion(const DevIn& in, int64_t zo, int64_t nzo, float* out, int iterations,
+                      float kappa, float dt, bool rational, float* b0, float* b1, cudaStream_t s,
+                      int64_t* launches) {
+  if (nzo <= 0) return cudaSuccess;
+  const int64_t plane = in.ny * in.nx, n = in.nz * plane;
+  const int g = grid_for(n);
+  switch (in.dt) {
+    case HB_U8: k_to_f32<uint8_t><<<g, kT, 0, s>>>((const uint8_t*)in.p, n, b0); break;
+    case HB_U16: k_to_f32<uint16_t><<<g, kT, 0, s>>>((const uint16_t*)in.p, n, b0); break;
+    case HB_U32: k_to_f32<uint32_t><<<g, kT, 0, s>>>((const uint32_t*)in.p, n, b0); break;
+    case HB_F32: k_to_f32<float><<<g, kT, 0, s>>>((const float*)in.p, n, b0); break;
+    default: return cudaErrorInvalidValue;
+  }
+  if (launches) *launches += 1;
+  for (int it = 0; it < iterations; ++it) {
+    k_diffusion_step<<<g, kT, 0, s>>>(b0, b1, (int)in.nz, (int)in.ny, (int)in.nx, kappa, dt, rational);
+    if (launches) *launches += 1;
+    float* t = b0;
+    b0 = b1;
+    b1 = t;
+  }
+  cudaError_t e = cudaMemcpyAsync(out, b0 + zo * plane, (size_t)(nzo * plane) * 4,
+                                  cudaMemcpyDeviceToDevice, s);
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
 
 cudaError_t lbp2d(const DevIn& in, int64_t zo, int64_t nzo, uint8_t* out, cudaStream_t s,
                   int64_t* launches) {

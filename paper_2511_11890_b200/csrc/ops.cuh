@@ -70,6 +70,11 @@ cudaError_t threshold(const DevIn& in, int64_t zo, int64_t nzo, uint32_t* out, d
                       cudaStream_t s, int64_t* launches);
 cudaError_t lbp2d(const DevIn& in, int64_t zo, int64_t nzo, uint8_t* out, cudaStream_t s,
                   int64_t* launches);
+// anisotropic diffusion over the whole block (closed faces, as the reference's
+// padded chunk), then slices [zo, zo+nzo) -> out; b0/b1: nz*ny*nx floats each
+cudaError_t diffusion(const DevIn& in, int64_t zo, int64_t nzo, float* out, int iterations,
+                      float kappa, float dt, bool rational, float* b0, float* b1, cudaStream_t s,
+                      int64_t* launches);
 // dtype conversion / copy (identity op, registry.py:127-133)
 cudaError_t copy_slices(const DevIn& in, int64_t zo, int64_t nzo, void* out,
                         cudaStream_t s, int64_t* launches);

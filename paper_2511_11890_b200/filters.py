@@ -116,6 +116,24 @@ def prewitt_program() -> _native.DeviceProgram:
     return _native.DeviceProgram([_native.Stage(_native.OP_PREWITT)])
 
 
+DIFFUSION_MODES = ("exponential", "rational")  # filters.py:17
+
+
+def diffusion_program(iterations, kappa, dt=1.0 / 6.0, mode="exponential") -> _native.DeviceProgram:
+    # filters.py:152-159 validation, same messages
+    if iterations < 1:
+        raise ParameterError(f"iterations must be >= 1, got {iterations}")
+    if not 0 < dt <= 1.0 / 6.0 + 1e-12:
+        raise ParameterError(f"dt must be in (0, 1/6], got {dt}")
+    if kappa <= 0:
+        raise ParameterError(f"kappa must be positive, got {kappa}")
+    if mode not in DIFFUSION_MODES:
+        raise ParameterError(f"mode must be one of {DIFFUSION_MODES}, got {mode!r}")
+    return _native.DeviceProgram([_native.Stage(
+        _native.OP_DIFFUSION, radius=int(iterations), sigma=float(kappa), amount=float(dt),
+        precision=DIFFUSION_MODES.index(mode))])
+
+
 def lbp2d_program() -> _native.DeviceProgram:
     return _native.DeviceProgram([_native.Stage(_native.OP_LBP2D)])
 
@@ -246,6 +264,13 @@ def hessian(data, sigma, precision="exact"):
 def sobel(data):
     """3D gradient magnitude with [1,2,1] cross-axis smoothing (filters.py:200-202)."""
     return apply_program(data, sobel_program())
+
+
+def anisotropic_diffusion(data, iterations, kappa, dt=1.0 / 6.0, mode="exponential"):
+    """Perona-Malik diffusion over the 6 axial neighbours (filters.py:142-184).
+    "rational" is bit-exact; "exponential" follows CUDA expf (<= 2 ulp per exp
+    from NumPy's float32 exp, which is itself a SIMD approximation)."""
+    return apply_program(data, diffusion_program(iterations, kappa, dt, mode))
 
 
 def lbp2d(data):

@@ -207,6 +207,11 @@ _map("sobel", {}, lambda p: OpProfile(halo_z=1, scratch_factor=12, out_dtype=FLO
      lambda p: filters.sobel_program())
 _map("prewitt", {}, lambda p: OpProfile(halo_z=1, scratch_factor=12, out_dtype=FLOAT32),
      lambda p: filters.prewitt_program())
+_map("anisotropic_diffusion",
+     {"iterations": (int, REQUIRED), "kappa": (float, REQUIRED), "dt": (float, 1.0 / 6.0),
+      "mode": (str, "exponential")},
+     lambda p: OpProfile(halo_z=p["iterations"], scratch_factor=12, out_dtype=FLOAT32),
+     lambda p: filters.diffusion_program(p["iterations"], p["kappa"], p["dt"], p["mode"]))
 _map("lbp2d", {}, lambda p: OpProfile(halo_z=0, scratch_factor=4, out_dtype=np.dtype("uint8")),
      lambda p: filters.lbp2d_program())
 _map("apply_threshold", {"t": (float, REQUIRED)},

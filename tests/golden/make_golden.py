@@ -87,6 +87,12 @@ def main():
         add(f"prewitt_{vol}", "prewitt", {}, vol, F.prewitt(vols[vol]))
     for vol in ("f32_a", "f32_thin", "f32_col", "u8_a", "u16_a", "bin_a", "f32_neg"):
         add(f"lbp2d_{vol}", "lbp2d", {}, vol, F.lbp2d(vols[vol]))
+    for vol in ("f32_unit", "u8_a", "f32_neg", "f32_col"):
+        for mode in F.DIFFUSION_MODES:
+            for it, kappa in ((1, 0.4), (3, 25.0)):
+                p = {"iterations": it, "kappa": kappa, "dt": 1.0 / 6.0, "mode": mode}
+                add(f"diffusion_{mode}_{vol}_{it}", "anisotropic_diffusion", p, vol,
+                    F.anisotropic_diffusion(vols[vol], it, kappa, 1.0 / 6.0, mode))
     for vol, ts in (("f32_unit", (0.1, 0.5)), ("u8_a", (127.5, 3.0)), ("u16_a", (30000.25,)),
                     ("f32_neg", (0.0, -12.3))):
         for t in ts:
@@ -131,7 +137,8 @@ def main():
                          ("hessian_xx", {"sigma": 2.0}), ("morph_erode", {"se": "ball:3"}),
                          ("morph_open", {"se": "ball:3", "iterations": 2}),
                          ("identity", {}), ("hessian_xy", {"sigma": 1.5}), ("sobel", {}),
-                         ("prewitt", {}), ("apply_threshold", {"t": 0.5}), ("lbp2d", {})]:
+                         ("prewitt", {}), ("apply_threshold", {"t": 0.5}), ("lbp2d", {}),
+                         ("anisotropic_diffusion", {"iterations": 3, "kappa": 10.0})]:
         op = R.get_operator(name)
         pr = op.profile(R.validate_params(op, params))
         profiles[name] = {"params": params, "halo_z": pr.halo_z, "scratch": pr.scratch_factor,
