@@ -187,6 +187,20 @@ int32_t hb_session_end(int32_t dev);
 /* Bytes currently reserved by the library's private pool on `dev`. */
 int64_t hb_device_pool_bytes(int32_t dev);
 
+/* Pass 1 of the two-pass global operators (chunking.py:282-306
+ * chunked_reduce) on the device, for Otsu (threshold.py:90-107).  `in` may be
+ * host (pinned or pageable; streamed in slabs) or device memory.
+ * hb_minmax: float32 volumes only (threshold.py:49-55); EPARAM if a NaN is
+ * present (the reference's range check raises).
+ * hb_histogram: np.histogram(data, bins, range=(lo, hi)) counts, bit-exact:
+ * values outside [lo, hi] are dropped, index = int(((v - lo) / (hi - lo)) *
+ * bins) with NumPy's edge corrections against `edges` (bins + 1 values of
+ * np.linspace(lo, hi, bins + 1, dtype=bin_type)); edges_f32 = 1 when bin_type
+ * is float32 (float32 data), else float64.  counts: bins int64, overwritten. */
+int32_t hb_minmax(const hb_volume* in, int32_t device, double* lo, double* hi);
+int32_t hb_histogram(const hb_volume* in, int32_t device, int32_t bins, double lo, double hi,
+                     const double* edges, int32_t edges_f32, int64_t* counts);
+
 /* Pinned-host helpers (cudaHostRegister for the duration of a job). */
 int32_t hb_pin(void* ptr, int64_t bytes);
 int32_t hb_unpin(void* ptr);

@@ -111,7 +111,7 @@ EXPORTS = (
     "hb_gaussian_radius", "hb_gaussian_weights", "hb_chain_halo", "hb_run",
     "hb_apply_device", "hb_chain_out_dtype", "hb_trim_device",
     "hb_device_pool_bytes", "hb_pin", "hb_unpin", "hb_last_error",
-    "hb_session_begin", "hb_session_end",
+    "hb_session_begin", "hb_session_end", "hb_minmax", "hb_histogram",
 )
 
 _lock = threading.Lock()
@@ -160,6 +160,12 @@ def load() -> ctypes.CDLL:
         L.hb_session_begin.restype = i32
         L.hb_session_end.argtypes = [i32]
         L.hb_session_end.restype = i32
+        L.hb_minmax.argtypes = [ctypes.POINTER(HbVolume), i32, ctypes.POINTER(ctypes.c_double),
+                                ctypes.POINTER(ctypes.c_double)]
+        L.hb_minmax.restype = i32
+        L.hb_histogram.argtypes = [ctypes.POINTER(HbVolume), i32, i32, ctypes.c_double,
+                                   ctypes.c_double, vp, i32, vp]
+        L.hb_histogram.restype = i32
         L.hb_pin.argtypes = [vp, i64]
         L.hb_pin.restype = i32
         L.hb_unpin.argtypes = [vp]
@@ -383,6 +389,39 @@ def trim_device(dev: Optional[int] = None) -> None:
 
 def device_pool_bytes(dev: Optional[int] = None) -> int:
     return int(load().hb_device_pool_bytes(current_device() if dev is None else int(dev)))
+
+
+def _volume_of(a):
+    """HbVolume view of a C-contiguous numpy array or CUDA torch tensor."""
+    if hasattr(a, "data_ptr"):
+        dt = np.dtype(str(a.dtype).replace("torch.", ""))
+        return HbVolume(a.data_ptr(), DTYPE_CODE[dt], HB_DEVICE, *a.shape), dt
+    return HbVolume(a.ctypes.data, DTYPE_CODE[a.dtype], HB_HOST, *a.shape), a.dtype
+
+
+def minmax(a, dev: Optional[int] = None):
+    """Device min/max of a float32 volume (hb_minmax)."""
+    L = load()
+    vol, _ = _volume_of(a)
+    lo, hi = ctypes.c_double(), ctypes.c_double()
+    rc = L.hb_minmax(ctypes.byref(vol), current_device() if dev is None else int(dev),
+                     ctypes.byref(lo), ctypes.byref(hi))
+    raise_for_status(rc, last_error())
+    return lo.value, hi.value
+
+
+def histogram(a, bins: int, lo: float, hi: float, edges: np.ndarray, edges_f32: bool,
+              dev: Optional[int] = None) -> np.ndarray:
+    """Device np.histogram counts (hb_histogram); int64[bins]."""
+    L = load()
+    vol, _ = _volume_of(a)
+    e = np.ascontiguousarray(edges, dtype=np.float64)
+    counts = np.empty(int(bins), np.int64)
+    rc = L.hb_histogram(ctypes.byref(vol), current_device() if dev is None else int(dev), int(bins),
+                        float(lo), float(hi), e.ctypes.data, 1 if edges_f32 else 0,
+                        counts.ctypes.data)
+    raise_for_status(rc, last_error())
+    return counts
 
 
 class session:

@@ -584,6 +584,71 @@ double now_ms() {
 // ===========================================================================
 // C ABI
 // ===========================================================================
+// ---------------------------------------------------------------------------
+// Two-pass global operators, pass 1 (chunking.py:282-306 chunked_reduce): the
+// volume streams through the device in bounded slabs (host volumes: pinned
+// DMA or the pinned ring) and `fn(device_ptr, n_voxels, stream)` folds each.
+// ---------------------------------------------------------------------------
+namespace {
+template <typename F>
+int32_t for_each_slab(const hb_volume* in, int32_t dev, F&& fn) {
+  if (!in || !in->data || in->nz < 0 || in->ny < 0 || in->nx < 0) {
+    set_err(nullptr, "bad volume");
+    return HB_EPARAM;
+  }
+  if (dev < 0 || dev >= hb_device_count()) {
+    set_err(nullptr, "no CUDA device " + std::to_string(dev));
+    return HB_EBUDGET_UNAVAILABLE;
+  }
+  std::lock_guard<std::mutex> lk(g_dev[dev].mu);
+  cudaSetDevice(dev);
+  cudaError_t e = ensure_pool(dev);
+  if (e != cudaSuccess) {
+    set_err(nullptr, cudaGetErrorString(e));
+    return HB_ECUDA;
+  }
+  const int64_t es = dtype_size(in->dtype);
+  const int64_t total = in->nz * in->ny * in->nx;
+  cudaStream_t s;
+  cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+  PoolAlloc pa{g_dev[dev].pool, s};
+  if (in->location == HB_DEVICE) {
+    e = fn(in->data, total, s);
+  } else {
+    const int64_t slab = std::max<int64_t>(1, (256ll << 20) / es);
+    void* buf = pa.get((size_t)std::min(total, slab) * es);
+    if (!buf) {
+      e = pa.err;
+    } else {
+      const bool pinned_in = is_pinned(in->data);
+      PinnedRing& ring = g_ring[dev];
+      if (!pinned_in) e = ring.init();
+      for (int64_t off = 0; off < total && e == cudaSuccess; off += slab) {
+        const int64_t n = std::min(slab, total - off);
+        const char* src = (const char*)in->data + off * es;
+        e = pinned_in ? cudaMemcpyAsync(buf, src, (size_t)(n * es), cudaMemcpyHostToDevice, s)
+                      : h2d_staged(ring, buf, src, (size_t)(n * es), s, auto_threads(0));
+        if (e == cudaSuccess) e = fn(buf, n, s);
+        // the single buffer is reused: the next copy is ordered after this
+        // fold on the same stream
+      }
+    }
+  }
+  cudaError_t se = cudaStreamSynchronize(s);
+  if (e == cudaSuccess) e = se;
+  pa.release();
+  cudaStreamSynchronize(s);
+  cudaStreamDestroy(s);
+  if (g_dev[dev].session.load() == 0) cudaMemPoolTrimTo(g_dev[dev].pool, 0);
+  if (e != cudaSuccess) {
+    set_err(nullptr, cudaGetErrorString(e));
+    cudaGetLastError();
+    return HB_ECUDA;
+  }
+  return HB_OK;
+}
+}  // namespace
+
 extern "C" {
 
 int32_t hb_abi_version(void) { return HB_ABI_VERSION; }
@@ -686,6 +751,72 @@ int32_t hb_session_end(int32_t dev) {
     return hb_trim_device(dev);
   }
   return HB_OK;
+}
+
+int32_t hb_minmax(const hb_volume* in, int32_t device, double* lo, double* hi) {
+  if (!in || in->dtype != HB_F32) {
+    set_err(nullptr, "hb_minmax: float32 volumes only (integer ranges are the dtype range)");
+    return HB_EUNSUPPORTED;
+  }
+  unsigned* acc = nullptr;
+  unsigned host[3] = {0xffffffffu, 0u, 0u};
+  int32_t rc = for_each_slab(in, device, [&](const void* p, int64_t n, cudaStream_t s) {
+    if (!acc) {
+      cudaError_t e = cudaMallocAsync(&acc, sizeof(host), s);
+      if (e != cudaSuccess) return e;
+      cudaMemcpyAsync(acc, host, sizeof(host), cudaMemcpyHostToDevice, s);
+    }
+    cudaError_t e = minmax_f32((const float*)p, n, acc, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(host, acc, sizeof(host), cudaMemcpyDeviceToHost, s);
+    return e;
+  });
+  if (acc) cudaFree(acc);
+  if (rc != HB_OK) return rc;
+  if (host[2] || host[0] > host[1]) {
+    set_err(nullptr, "autodetected histogram range is not finite (NaN or empty volume)");
+    return HB_EPARAM;
+  }
+  auto unkey = [](unsigned k) {
+    const unsigned u = (k & 0x80000000u) ? (k & 0x7fffffffu) : ~k;
+    float f;
+    std::memcpy(&f, &u, 4);
+    return (double)f;
+  };
+  if (lo) *lo = unkey(host[0]);
+  if (hi) *hi = unkey(host[1]);
+  return HB_OK;
+}
+
+int32_t hb_histogram(const hb_volume* in, int32_t device, int32_t bins, double lo, double hi,
+                     const double* edges, int32_t edges_f32, int64_t* counts) {
+  if (!in || bins < 1 || !edges || !counts || !(hi > lo) || !std::isfinite(lo) || !std::isfinite(hi)) {
+    set_err(nullptr, "hb_histogram: bins >= 1, finite lo < hi and edges/counts required");
+    return HB_EPARAM;
+  }
+  double* d_edges = nullptr;
+  unsigned long long* d_counts = nullptr;
+  int32_t rc = for_each_slab(in, device, [&](const void* p, int64_t n, cudaStream_t s) {
+    if (!d_counts) {
+      cudaError_t e = cudaMallocAsync(&d_counts, sizeof(unsigned long long) * bins, s);
+      if (e == cudaSuccess) e = cudaMallocAsync(&d_edges, sizeof(double) * (bins + 1), s);
+      if (e != cudaSuccess) return e;
+      cudaMemsetAsync(d_counts, 0, sizeof(unsigned long long) * bins, s);
+      cudaMemcpyAsync(d_edges, edges, sizeof(double) * (bins + 1), cudaMemcpyHostToDevice, s);
+    }
+    return histogram(p, in->dtype, n, bins, lo, hi, d_edges, edges_f32 != 0, d_counts, s);
+  });
+  if (rc == HB_OK && d_counts) {
+    cudaError_t e = cudaMemcpy(counts, d_counts, sizeof(unsigned long long) * bins, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) {
+      set_err(nullptr, cudaGetErrorString(e));
+      rc = HB_ECUDA;
+    }
+  } else if (rc == HB_OK) {
+    std::memset(counts, 0, sizeof(int64_t) * bins);
+  }
+  if (d_counts) cudaFree(d_counts);
+  if (d_edges) cudaFree(d_edges);
+  return rc;
 }
 
 int64_t hb_device_pool_bytes(int32_t dev) {

@@ -97,6 +97,16 @@ cudaError_t mean_fused(const DevIn& in, int64_t zo, int64_t nzo, float* out, int
 cudaError_t mean_stream(const DevIn& in, int64_t zo, int64_t nzo, float* out, int r,
                         cudaStream_t s, int64_t* launches);
 
+// --- two-pass global operators, pass 1 (reduce.cu) ---------------------------
+// acc: 3 unsigned on the device, initialised {~0u, 0, 0}: ordered-key min,
+// max, NaN flag
+cudaError_t minmax_f32(const float* p, int64_t n, unsigned* acc, cudaStream_t s);
+// np.histogram counts (accumulated into counts[bins]); edges: bins+1 doubles
+// on the device
+cudaError_t histogram(const void* p, int dt, int64_t n, int bins, double lo, double hi,
+                      const double* edges, bool edges_f32, unsigned long long* counts,
+                      cudaStream_t s);
+
 // --- median (median.cu) ----------------------------------------------------
 cudaError_t median(const DevIn& in, int64_t zo, int64_t nzo, void* out, int r,
                    cudaStream_t s, int64_t* launches);

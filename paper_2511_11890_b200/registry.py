@@ -109,6 +109,8 @@ def run_operator(
     params = validate_params(op, params or {}) if validate else dict(params or {})
     if budget is None:
         budget = profile_budget()
+    if op.kind == "global":  # registry.py:99-103: global operators run themselves
+        return op.run(data, params, budget, cancel)
     program = _program_for(op, params)
     arr, restore = filters.coerce_input(data, program)
     out, report = execute_chunked(arr, program, op.profile(params), budget, params,
@@ -120,6 +122,9 @@ def run_direct(data: np.ndarray, name: str, params: Optional[dict] = None, aux=N
     """Whole-volume single-shot evaluation (registry.py:106-114)."""
     op = get_operator(name)
     params = validate_params(op, params or {})
+    if op.kind == "global":
+        result, _ = op.run(data, params, None, None)
+        return result
     return op.fn(data, params, aux or {})
 
 
@@ -217,6 +222,25 @@ _map("lbp2d", {}, lambda p: OpProfile(halo_z=0, scratch_factor=4, out_dtype=np.d
 _map("apply_threshold", {"t": (float, REQUIRED)},
      lambda p: OpProfile(halo_z=0, scratch_factor=6, out_dtype=LABEL_DTYPE),
      lambda p: filters.threshold_program(p["t"]), output="labels")
+
+# global Otsu (registry.py:312-334): two passes, device histogram + apply
+def _run_otsu(data, params, budget, cancel):
+    from . import threshold
+    from .ledger import LEDGER
+
+    LEDGER.job_start()
+    out, t = threshold.otsu_binarize(data, params.get("bins", 256), budget, cancel=cancel)
+    report = ExecutionReport(chunk_count=1)
+    if budget is not None:
+        snap = LEDGER.snapshot()
+        report.peak_bytes = snap.peak_bytes - snap.baseline_bytes
+        report.residual_bytes = snap.residual_bytes
+    report.threshold = t
+    return out, report
+
+
+register(Operator(name="otsu", kind="global", output="labels", schema={"bins": (int, 256)},
+                  run=_run_otsu))
 
 # LoG = hessian trace; profile as the reference's hessian_* (registry.py:234-246)
 _map("log",

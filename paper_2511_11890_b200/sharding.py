@@ -123,3 +123,57 @@ def run_sharded(local, program, rank: int, world: int, group=None,
         padded, lo, hi = exchange_halos(cur, h, rank, world, group)
         cur = apply_block(padded, prog, lo, padded.shape[0] - lo - hi)
     return cur
+
+
+# ---------------------------------------------------------------------------
+# Two-pass global operator across ranks: Otsu (threshold.py:90-131).
+# Pass 1 is the one place the path has a real exchange: each rank reduces its
+# own slab on its GPU, then the float range (min/max) and the int64 histogram
+# are all-reduced (NCCL over NVLink on the box, gloo in the CPU tests); every
+# rank finalises the same threshold and applies it to its slab locally.
+# ---------------------------------------------------------------------------
+def otsu_sharded(local, bins: int, rank: int, world: int, group=None,
+                 minmax_fn: Optional[Callable] = None, hist_fn: Optional[Callable] = None,
+                 apply_fn: Optional[Callable] = None):
+    """Return (labels of this rank's slab, threshold) — identical on every
+    rank to the single-volume otsu_binarize.  ``local``: this rank's slab
+    (numpy or CUDA tensor); the hooks default to the device
+    (threshold.data_minmax / compute_histogram / apply_threshold)."""
+    import torch
+
+    from . import threshold
+
+    minmax_fn = minmax_fn or threshold.data_minmax
+    hist_fn = hist_fn or (lambda a, b, r: threshold.compute_histogram(a, b, r).counts)
+    apply_fn = apply_fn or threshold.apply_threshold
+    dt = np.dtype(str(local.dtype).replace("torch.", ""))
+    if np.issubdtype(dt, np.integer):
+        lim = np.iinfo(dt)
+        lo, hi = float(lim.min), float(lim.max) + 1.0
+    else:
+        lo, hi = minmax_fn(local)
+        if world > 1:  # min of the mins, max of the maxes (chunked_reduce, threshold.py:100-101)
+            dist = _dist()
+            dev = _comm_device(group)
+            lo_t = torch.tensor([lo], dtype=torch.float64, device=dev)
+            hi_t = torch.tensor([hi], dtype=torch.float64, device=dev)
+            dist.all_reduce(lo_t, op=dist.ReduceOp.MIN, group=group)
+            dist.all_reduce(hi_t, op=dist.ReduceOp.MAX, group=group)
+            lo, hi = float(lo_t.item()), float(hi_t.item())
+        if lo == hi:
+            hi = lo + 1.0
+    counts = np.asarray(hist_fn(local, bins, (lo, hi)), dtype=np.int64)
+    if world > 1:
+        dist = _dist()
+        c = torch.from_numpy(counts.copy()).to(_comm_device(group))
+        dist.all_reduce(c, op=dist.ReduceOp.SUM, group=group)
+        counts = c.cpu().numpy()
+    t = threshold.otsu_from_histogram(threshold.Histogram(lo, hi, counts))
+    return apply_fn(local, t), t
+
+
+def _comm_device(group):
+    import torch
+
+    backend = _dist().get_backend(group)
+    return torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu")

@@ -87,6 +87,16 @@ def main():
         add(f"prewitt_{vol}", "prewitt", {}, vol, F.prewitt(vols[vol]))
     for vol in ("f32_a", "f32_thin", "f32_col", "u8_a", "u16_a", "bin_a", "f32_neg"):
         add(f"lbp2d_{vol}", "lbp2d", {}, vol, F.lbp2d(vols[vol]))
+    # global Otsu (registry.py:312-334): binarized output; threshold in meta
+    otsu_t = {}
+    for vol in ("f32_a", "f32_unit", "u8_a", "u16_a", "f32_neg", "bin_a"):
+        for bins in (256, 64):
+            try:
+                lab, t = T.otsu_binarize(vols[vol], bins)
+            except ref.errors.HarpiaError:  # degenerate histogram (e.g. binary u8, 64 bins)
+                continue
+            add(f"otsu_{vol}_{bins}", "otsu", {"bins": bins}, vol, lab)
+            otsu_t[f"otsu_{vol}_{bins}"] = t
     for vol in ("f32_unit", "u8_a", "f32_neg", "f32_col"):
         for mode in F.DIFFUSION_MODES:
             for it, kappa in ((1, 0.4), (3, 25.0)):
@@ -159,7 +169,7 @@ def main():
     np.savez_compressed(HERE / "golden_arrays.npz", **arrays)
     meta = {"generator": "tests/golden/make_golden.py", "reference": args.ref,
             "cases": cases, "plans": plans, "profiles": profiles, "weights": weights,
-            "ball_sizes": balls, "sidecars": sidecars}
+            "ball_sizes": balls, "sidecars": sidecars, "otsu_thresholds": otsu_t}
     (HERE / "golden_meta.json").write_text(json.dumps(meta, indent=1))
     print(f"{len(cases)} cases, {sum(a.nbytes for a in arrays.values())} bytes raw")
 

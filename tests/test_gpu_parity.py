@@ -375,3 +375,33 @@ def test_anisotropic_diffusion_vs_oracle(hb, oracle):
             assert np.array_equal(r, oracle.anisotropic_diffusion(x, it, kappa, 1.0 / 6.0, "rational"))
             e = filters.anisotropic_diffusion(x, it, kappa)
             assert float_close(e, oracle.anisotropic_diffusion(x, it, kappa)) <= FLOAT_TOL
+
+
+def test_otsu_two_pass_on_device(hb, oracle, golden):
+    """Global Otsu (threshold.py:90-131) through the device: the histogram is
+    np.histogram bit for bit, the threshold is the reference's, and the
+    chunked apply pass equals the direct one."""
+    from conftest import budget_for
+    from paper_2511_11890_b200 import registry, threshold
+
+    meta, arrays = golden
+    for name, t_ref in meta["otsu_thresholds"].items():
+        case = next(c for c in meta["cases"] if c["name"] == name)
+        assert threshold.otsu(arrays[case["input"]], case["params"]["bins"]) == t_ref, name
+    rng = np.random.default_rng(8)
+    for shape, dt in (((40, 67, 129), "f32"), ((7, 256, 64), "u16"), ((33, 1, 300), "u8")):
+        x = _vol(rng, shape, dt)
+        if dt == "f32":
+            x = x * 3.5 - 1.0
+        r = threshold.histogram_range(x)
+        assert r == oracle.histogram_range(x)
+        for bins in (256, 37):
+            np.testing.assert_array_equal(threshold.compute_histogram(x, bins, r).counts,
+                                          oracle.histogram(x, bins, r))
+        direct = registry.run_direct(x, "otsu", {})
+        op = registry.get_operator("apply_threshold")
+        prof = op.profile({"t": 0.0})
+        chunked, rep = registry.run_operator(x, "otsu", {}, budget_for(prof, x.shape, np.dtype(np.uint32), 4))
+        assert np.array_equal(direct, chunked) and direct.dtype == np.uint32
+        assert rep.threshold == oracle.otsu(x)
+        assert np.array_equal(direct, oracle.apply_threshold(x, oracle.otsu(x)))

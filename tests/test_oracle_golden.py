@@ -77,3 +77,14 @@ def test_gaussian_impulse_is_separable_kernel(oracle):
     r = (k.size - 1) // 2
     exp = k[:, None, None] * k[None, :, None] * k[None, None, :]
     assert np.max(np.abs(out[8 - r:9 + r, 8 - r:9 + r, 8 - r:9 + r] - exp)) <= 1e-6
+
+
+def test_otsu_thresholds_match_reference(golden, oracle):
+    """threshold.py:90-107 (np.histogram + the between-class-variance split):
+    the restated histogram and split give the reference's threshold exactly."""
+    meta, arrays = golden
+    for case in meta["cases"]:
+        if case["op"] != "otsu":
+            continue
+        x = arrays[case["input"]]
+        assert oracle.otsu(x, case["params"]["bins"]) == meta["otsu_thresholds"][case["name"]], case["name"]

@@ -119,3 +119,44 @@ def test_partition():
     assert [(s.z0, s.z1) for s in slabs] == [(0, 4), (4, 7), (7, 10)]
     with pytest.raises(ValueError):
         sharding.partition(2, 3)
+
+
+def _otsu_worker(rank, world, port, kind, outdir):
+    sys.path.insert(0, ROOT)
+    from oracle import oracle as O
+    from paper_2511_11890_b200 import sharding
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    try:
+        vol = _volume(kind)
+        if kind == "f32":
+            vol = vol * 7.0 - 2.0
+        me = sharding.partition(vol.shape[0], world)[rank]
+        local = np.ascontiguousarray(vol[me.z0:me.z1])
+        labels, t = sharding.otsu_sharded(
+            local, 64, rank, world,
+            minmax_fn=lambda a: (float(a.min()), float(a.max())),
+            hist_fn=lambda a, b, r: O.histogram(a, b, r),
+            apply_fn=lambda a, tt: O.apply_threshold(a, tt))
+        np.save(os.path.join(outdir, f"otsu{rank}.npy"), labels)
+        np.save(os.path.join(outdir, f"t{rank}.npy"), np.array([t]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("kind", ["f32", "u16"])
+def test_otsu_sharded_equals_whole(kind, oracle):
+    """Pass 1 all-reduces the range and the int64 histogram across ranks; the
+    stitched labels and the threshold equal the single-volume Otsu."""
+    world = 2
+    vol = _volume(kind)
+    if kind == "f32":
+        vol = vol * 7.0 - 2.0
+    t_whole = oracle.otsu(vol, 64)
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_otsu_worker, args=(world, _free_port(), kind, d), nprocs=world, join=True)
+        got = np.concatenate([np.load(os.path.join(d, f"otsu{r}.npy")) for r in range(world)])
+        ts = [float(np.load(os.path.join(d, f"t{r}.npy"))[0]) for r in range(world)]
+    assert ts == [t_whole] * world
+    assert np.array_equal(got, oracle.apply_threshold(vol, t_whole))
