@@ -201,6 +201,13 @@ int32_t hb_minmax(const hb_volume* in, int32_t device, double* lo, double* hi);
 int32_t hb_histogram(const hb_volume* in, int32_t device, int32_t bins, double lo, double hi,
                      const double* edges, int32_t edges_f32, int64_t* counts);
 
+/* Connected-components labelling (quantify.py:60-111): labels 1..count in
+ * first-voxel scan order (uint32, `out`), background 0; connectivity 6 or 26;
+ * the volume must fit in device memory (< 2^31 voxels).  `in`/`out` host or
+ * device; any nonzero voxel is foreground. */
+int32_t hb_connected_components(const hb_volume* in, hb_volume* out, int32_t connectivity,
+                                int32_t device, int64_t* count);
+
 /* Pinned-host helpers (cudaHostRegister for the duration of a job). */
 int32_t hb_pin(void* ptr, int64_t bytes);
 int32_t hb_unpin(void* ptr);

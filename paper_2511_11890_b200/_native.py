@@ -112,6 +112,7 @@ EXPORTS = (
     "hb_apply_device", "hb_chain_out_dtype", "hb_trim_device",
     "hb_device_pool_bytes", "hb_pin", "hb_unpin", "hb_last_error",
     "hb_session_begin", "hb_session_end", "hb_minmax", "hb_histogram",
+    "hb_connected_components",
 )
 
 _lock = threading.Lock()
@@ -166,6 +167,9 @@ def load() -> ctypes.CDLL:
         L.hb_histogram.argtypes = [ctypes.POINTER(HbVolume), i32, i32, ctypes.c_double,
                                    ctypes.c_double, vp, i32, vp]
         L.hb_histogram.restype = i32
+        L.hb_connected_components.argtypes = [ctypes.POINTER(HbVolume), ctypes.POINTER(HbVolume),
+                                              i32, i32, ctypes.POINTER(ctypes.c_int64)]
+        L.hb_connected_components.restype = i32
         L.hb_pin.argtypes = [vp, i64]
         L.hb_pin.restype = i32
         L.hb_unpin.argtypes = [vp]

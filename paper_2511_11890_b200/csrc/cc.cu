@@ -1,0 +1,158 @@
+// cc.cu — connected-components labelling (quantify.py:60-111) on the device.
+//
+// The reference labels a binary mask (ndimage.label, 6- or 26-connectivity)
+// and compacts the ids to 1..count in first-voxel scan order (quantify.py:
+// 48-57), so its output is canonical: any correct partition into components,
+// numbered by first occurrence, reproduces it exactly.  Here:
+//   init     : every foreground voxel is its own root (label = linear index)
+//   union    : each foreground voxel unions with its already-scanned
+//              neighbours (smaller linear index) through a lock-free
+//              union-find whose links always point to the smaller root
+//              (atomicMin), so a component's final root is its smallest index
+//              = its first voxel in scan order
+//   flatten  : label = root
+//   compact  : roots flagged, exclusive prefix sum (CUB) -> 1..count in root
+//              order = first-occurrence order; every voxel takes its root's id
+// Volumes up to 2^31 - 1 voxels (int32 labels), resident in HBM.
+#include <cuda_runtime.h>
+
+#include <cub/device/device_scan.cuh>
+
+#include "ops.cuh"
+
+namespace hb {
+namespace {
+
+constexpr int kCT = 256;
+
+inline int cgrid(int64_t n) {
+  const int64_t b = (n + kCT - 1) / kCT, cap = (int64_t)kNumSMs * 16;
+  return (int)(b < 1 ? 1 : (b < cap ? b : cap));
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kCT) k_cc_init(const T* __restrict__ in, int n, int* __restrict__ lab) {
+  for (int i = blockIdx.x * kCT + threadIdx.x; i < n; i += gridDim.x * kCT)
+    lab[i] = in[i] != T(0) ? i : -1;
+}
+
+// plain find (path halving here broke the scan-order roots on the B200 in
+// testing; the flatten pass below compresses every path once instead)
+__device__ __forceinline__ int cc_find(const int* lab, int x) {
+  int p = lab[x];
+  while (p != x) {
+    x = p;
+    p = lab[x];
+  }
+  return x;
+}
+
+// link the larger root under the smaller one; retry when another thread moved it
+__device__ __forceinline__ void cc_union(int* lab, int a, int b) {
+  while (true) {
+    a = cc_find(lab, a);
+    b = cc_find(lab, b);
+    if (a == b) return;
+    if (a > b) {
+      const int t = a;
+      a = b;
+      b = t;
+    }
+    const int old = atomicMin(&lab[b], a);
+    if (old == b) return;
+    b = old;
+  }
+}
+
+template <int CONN>
+__global__ void __launch_bounds__(kCT) k_cc_union(int* __restrict__ lab, int nz, int ny, int nx) {
+  const int plane = ny * nx, n = nz * plane;
+  for (int i = blockIdx.x * kCT + threadIdx.x; i < n; i += gridDim.x * kCT) {
+    if (lab[i] < 0) continue;
+    const int z = i / plane, r = i - z * plane, y = r / nx, x = r - y * nx;
+    if (CONN == 6) {
+      if (x > 0 && lab[i - 1] >= 0) cc_union(lab, i, i - 1);
+      if (y > 0 && lab[i - nx] >= 0) cc_union(lab, i, i - nx);
+      if (z > 0 && lab[i - plane] >= 0) cc_union(lab, i, i - plane);
+    } else {
+      // the 13 neighbours that precede i in scan order
+#pragma unroll
+      for (int dz = -1; dz <= 0; ++dz)
+#pragma unroll
+        for (int dy = -1; dy <= 1; ++dy)
+#pragma unroll
+          for (int dx = -1; dx <= 1; ++dx) {
+            if (dz == 0 && (dy > 0 || (dy == 0 && dx >= 0))) continue;
+            const int zz = z + dz, yy = y + dy, xx = x + dx;
+            if (zz < 0 || yy < 0 || yy >= ny || xx < 0 || xx >= nx) continue;
+            const int j = i + dz * plane + dy * nx + dx;
+            if (lab[j] >= 0) cc_union(lab, i, j);
+          }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kCT) k_cc_flatten(int* __restrict__ lab, int* __restrict__ flag, int n) {
+  for (int i = blockIdx.x * kCT + threadIdx.x; i < n; i += gridDim.x * kCT) {
+    const int l = lab[i];
+    int root = -1;
+    if (l >= 0) root = cc_find(lab, i);
+    flag[i] = (l >= 0 && root == i) ? 1 : 0;
+    // roots are final after the union kernel: writing them back is safe
+    if (l >= 0) lab[i] = root;
+  }
+}
+
+__global__ void __launch_bounds__(kCT)
+k_cc_relabel(const int* __restrict__ lab, const int* __restrict__ ids, int n, uint32_t* __restrict__ out) {
+  for (int i = blockIdx.x * kCT + threadIdx.x; i < n; i += gridDim.x * kCT) {
+    const int l = lab[i];
+    out[i] = l >= 0 ? (uint32_t)(ids[l] + 1) : 0u;
+  }
+}
+
+}  // namespace
+
+cudaError_t connected_components(const void* in, int dt, int64_t nz, int64_t ny, int64_t nx,
+                                 int conn, uint32_t* out, int* lab, int* flag, int* ids,
+                                 void* scan_tmp, size_t scan_bytes, int64_t* count, cudaStream_t s) {
+  const int64_t n64 = nz * ny * nx;
+  if (n64 <= 0) {
+    if (count) *count = 0;
+    return cudaSuccess;
+  }
+  if (n64 >= (1ll << 31) - 1) return cudaErrorNotSupported;
+  const int n = (int)n64;
+  const int g = cgrid(n64);
+  switch (dt) {
+    case HB_U8: k_cc_init<uint8_t><<<g, kCT, 0, s>>>((const uint8_t*)in, n, lab); break;
+    case HB_U16: k_cc_init<uint16_t><<<g, kCT, 0, s>>>((const uint16_t*)in, n, lab); break;
+    case HB_U32: k_cc_init<uint32_t><<<g, kCT, 0, s>>>((const uint32_t*)in, n, lab); break;
+    case HB_F32: k_cc_init<float><<<g, kCT, 0, s>>>((const float*)in, n, lab); break;
+    default: return cudaErrorInvalidValue;
+  }
+  if (conn == 6) k_cc_union<6><<<g, kCT, 0, s>>>(lab, (int)nz, (int)ny, (int)nx);
+  else k_cc_union<26><<<g, kCT, 0, s>>>(lab, (int)nz, (int)ny, (int)nx);
+  k_cc_flatten<<<g, kCT, 0, s>>>(lab, flag, n);
+  size_t need = scan_bytes;
+  cudaError_t e = cub::DeviceScan::ExclusiveSum(scan_tmp, need, flag, ids, n, s);
+  if (e != cudaSuccess) return e;
+  k_cc_relabel<<<g, kCT, 0, s>>>(lab, ids, n, out);
+  if (count) {
+    int last_id = 0, last_flag = 0;
+    cudaMemcpyAsync(&last_id, ids + n - 1, 4, cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(&last_flag, flag + n - 1, 4, cudaMemcpyDeviceToHost, s);
+    e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return e;
+    *count = (int64_t)last_id + last_flag;
+  }
+  return cudaGetLastError();
+}
+
+size_t connected_components_scan_bytes(int64_t n) {
+  size_t bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, bytes, (int*)nullptr, (int*)nullptr, (int)n);
+  return bytes;
+}
+
+}  // namespace hb

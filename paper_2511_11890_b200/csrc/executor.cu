@@ -787,6 +787,74 @@ int32_t hb_minmax(const hb_volume* in, int32_t device, double* lo, double* hi) {
   return HB_OK;
 }
 
+int32_t hb_connected_components(const hb_volume* in, hb_volume* out, int32_t connectivity,
+                                int32_t device, int64_t* count) {
+  if (!in || !out || !in->data || !out->data || out->dtype != HB_U32 || in->nz != out->nz ||
+      in->ny != out->ny || in->nx != out->nx) {
+    set_err(nullptr, "hb_connected_components: uint32 output of the input's shape required");
+    return HB_EPARAM;
+  }
+  if (connectivity != 6 && connectivity != 26) {
+    set_err(nullptr, "connectivity must be 6 or 26, got " + std::to_string(connectivity));
+    return HB_EPARAM;
+  }
+  if (device < 0 || device >= hb_device_count()) {
+    set_err(nullptr, "no CUDA device " + std::to_string(device));
+    return HB_EBUDGET_UNAVAILABLE;
+  }
+  const int64_t n = in->nz * in->ny * in->nx;
+  if (n >= (1ll << 31) - 1) {
+    set_err(nullptr, "connected components: volumes of 2^31 voxels or more are not supported");
+    return HB_EUNSUPPORTED;
+  }
+  std::lock_guard<std::mutex> lk(g_dev[device].mu);
+  cudaSetDevice(device);
+  cudaError_t e = ensure_pool(device);
+  if (e != cudaSuccess) {
+    set_err(nullptr, cudaGetErrorString(e));
+    return HB_ECUDA;
+  }
+  cudaStream_t s;
+  cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+  PoolAlloc pa{g_dev[device].pool, s};
+  const size_t es = (size_t)dtype_size(in->dtype), nn = (size_t)std::max<int64_t>(n, 1);
+  const size_t scan_bytes = connected_components_scan_bytes(n) + 256;
+  const void* d_in = in->data;
+  uint32_t* d_out = (uint32_t*)out->data;
+  int* lab = (int*)pa.get(nn * 4);
+  int* flag = (int*)pa.get(nn * 4);
+  int* ids = (int*)pa.get(nn * 4);
+  void* tmp = pa.get(scan_bytes);
+  if (in->location != HB_DEVICE && lab) {
+    void* buf = pa.get(nn * es);
+    if (buf) {
+      e = cudaMemcpyAsync(buf, in->data, (size_t)n * es, cudaMemcpyHostToDevice, s);
+      d_in = buf;
+    }
+  }
+  if (out->location != HB_DEVICE && lab) d_out = (uint32_t*)pa.get(nn * 4);
+  if (!lab || !flag || !ids || !tmp || !d_out || pa.err != cudaSuccess) e = pa.err != cudaSuccess ? pa.err : cudaErrorMemoryAllocation;
+  int64_t cnt = 0;
+  if (e == cudaSuccess)
+    e = connected_components(d_in, in->dtype, in->nz, in->ny, in->nx, connectivity, d_out, lab,
+                             flag, ids, tmp, scan_bytes, &cnt, s);
+  if (e == cudaSuccess && out->location != HB_DEVICE)
+    e = cudaMemcpyAsync(out->data, d_out, (size_t)n * 4, cudaMemcpyDeviceToHost, s);
+  cudaError_t se = cudaStreamSynchronize(s);
+  if (e == cudaSuccess) e = se;
+  pa.release();
+  cudaStreamSynchronize(s);
+  cudaStreamDestroy(s);
+  if (g_dev[device].session.load() == 0) cudaMemPoolTrimTo(g_dev[device].pool, 0);
+  if (e != cudaSuccess) {
+    set_err(nullptr, std::string("connected components: ") + cudaGetErrorString(e));
+    cudaGetLastError();
+    return e == cudaErrorMemoryAllocation ? HB_EBUDGET_UNAVAILABLE : HB_ECUDA;
+  }
+  if (count) *count = cnt;
+  return HB_OK;
+}
+
 int32_t hb_histogram(const hb_volume* in, int32_t device, int32_t bins, double lo, double hi,
                      const double* edges, int32_t edges_f32, int64_t* counts) {
   if (!in || bins < 1 || !edges || !counts || !(hi > lo) || !std::isfinite(lo) || !std::isfinite(hi)) {

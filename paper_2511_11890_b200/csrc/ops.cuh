@@ -107,6 +107,12 @@ cudaError_t histogram(const void* p, int dt, int64_t n, int bins, double lo, dou
                       const double* edges, bool edges_f32, unsigned long long* counts,
                       cudaStream_t s);
 
+// --- connected components (cc.cu) --------------------------------------------
+cudaError_t connected_components(const void* in, int dt, int64_t nz, int64_t ny, int64_t nx,
+                                 int conn, uint32_t* out, int* lab, int* flag, int* ids,
+                                 void* scan_tmp, size_t scan_bytes, int64_t* count, cudaStream_t s);
+size_t connected_components_scan_bytes(int64_t n);
+
 // --- median (median.cu) ----------------------------------------------------
 cudaError_t median(const DevIn& in, int64_t zo, int64_t nzo, void* out, int r,
                    cudaStream_t s, int64_t* launches);

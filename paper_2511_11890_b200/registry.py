@@ -242,6 +242,22 @@ def _run_otsu(data, params, budget, cancel):
 register(Operator(name="otsu", kind="global", output="labels", schema={"bins": (int, 256)},
                   run=_run_otsu))
 
+
+# connected components (registry.py:337-351) on the device
+def _run_cc(data, params, budget, cancel):
+    from . import quantify
+    from .ledger import LEDGER
+
+    LEDGER.job_start()
+    labels, count = quantify.connected_components(data, params["connectivity"], budget)
+    report = ExecutionReport(chunk_count=1)
+    report.component_count = count
+    return labels, report
+
+
+register(Operator(name="connected_components", kind="global", output="labels",
+                  schema={"connectivity": (int, 6)}, run=_run_cc))
+
 # LoG = hessian trace; profile as the reference's hessian_* (registry.py:234-246)
 _map("log",
      {"sigma": (float, REQUIRED), "precision": (_precision_param, "exact")},

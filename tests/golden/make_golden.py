@@ -87,6 +87,12 @@ def main():
         add(f"prewitt_{vol}", "prewitt", {}, vol, F.prewitt(vols[vol]))
     for vol in ("f32_a", "f32_thin", "f32_col", "u8_a", "u16_a", "bin_a", "f32_neg"):
         add(f"lbp2d_{vol}", "lbp2d", {}, vol, F.lbp2d(vols[vol]))
+    # connected components (registry.py:337-351): canonical labels
+    Q = ref.quantify
+    for vol in ("bin_a", "u8_a", "f32_thin", "f32_col"):
+        for conn in (6, 26):
+            lab, _n = Q.connected_components(vols[vol], conn)
+            add(f"cc_{vol}_{conn}", "connected_components", {"connectivity": conn}, vol, lab)
     # global Otsu (registry.py:312-334): binarized output; threshold in meta
     otsu_t = {}
     for vol in ("f32_a", "f32_unit", "u8_a", "u16_a", "f32_neg", "bin_a"):

@@ -405,3 +405,30 @@ def test_otsu_two_pass_on_device(hb, oracle, golden):
         assert np.array_equal(direct, chunked) and direct.dtype == np.uint32
         assert rep.threshold == oracle.otsu(x)
         assert np.array_equal(direct, oracle.apply_threshold(x, oracle.otsu(x)))
+
+
+@pytest.mark.parametrize("conn", [6, 26])
+def test_connected_components_vs_oracle(hb, oracle, conn):
+    """quantify.py:60-111: canonical labels (1..count, first-voxel scan order)
+    bit-exact, on ragged shapes and densities around the percolation point,
+    host and device inputs; the registry's chunked run gives the same labels."""
+    import torch
+
+    from conftest import budget_for
+    from paper_2511_11890_b200 import quantify, registry
+    from paper_2511_11890_b200.chunking import OpProfile
+
+    rng = np.random.default_rng(conn)
+    for shape in ((40, 67, 129), (1, 1, 9), (64, 64, 64), (9, 200, 3)):
+        for dens in (0.15, 0.3, 0.6):
+            m = (rng.random(shape) < dens).astype(np.uint8)
+            want, n = oracle.connected_components(m, conn)
+            got, k = quantify.connected_components(m, conn)
+            assert k == n and got.dtype == np.uint32 and np.array_equal(got, want), (shape, dens)
+    m = (rng.random((96, 80, 72)) < 0.3)
+    want, n = oracle.connected_components(m.astype(np.uint8), conn)
+    dev, k = quantify.connected_components(torch.from_numpy(m).cuda(), conn)
+    assert k == n and np.array_equal(dev.cpu().numpy(), want)
+    lab, rep = registry.run_operator(m.astype(np.uint8), "connected_components", {"connectivity": conn},
+                                     budget_for(OpProfile(0, 6), m.shape, np.uint8, 4))
+    assert rep.component_count == n and np.array_equal(lab, want)

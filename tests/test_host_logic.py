@@ -81,7 +81,8 @@ class TestRegistry:
             "morph_erode", "morph_dilate", "morph_open", "morph_close",
             # SURVEY.md §8(f) row 2
             "hessian_xx", "hessian_yy", "hessian_zz", "hessian_xy", "hessian_xz", "hessian_yz",
-            "sobel", "prewitt", "apply_threshold", "lbp2d", "anisotropic_diffusion", "otsu"}
+            "sobel", "prewitt", "apply_threshold", "lbp2d", "anisotropic_diffusion", "otsu",
+            "connected_components"}
 
     def test_profiles_match_reference(self, golden):
         meta, _ = golden
