@@ -10,7 +10,7 @@
 //              union-find whose links always point to the smaller root
 //              (atomicMin), so a component's final root is its smallest index
 //              = its first voxel in scan order
-//   flatten  : label = root
+//   flatten  : root of every voxel (path halving) into the output buffer
 //   compact  : roots flagged, exclusive prefix sum (CUB) -> 1..count in root
 //              order = first-occurrence order; every voxel takes its root's id
 // Volumes up to 2^31 - 1 voxels (int32 labels), resident in HBM.
@@ -36,13 +36,17 @@ __global__ void __launch_bounds__(kCT) k_cc_init(const T* __restrict__ in, int n
     lab[i] = in[i] != T(0) ? i : -1;
 }
 
-// plain find (path halving here broke the scan-order roots on the B200 in
-// testing; the flatten pass below compresses every path once instead)
-__device__ __forceinline__ int cc_find(const int* lab, int x) {
+// find with path halving: a link is only ever rewritten while its node is a
+// non-root, and always to an ancestor, so racing (even stale) halving stores
+// keep the partition and never touch a root — the smallest index of every
+// component stays its root
+__device__ __forceinline__ int cc_find(int* lab, int x) {
   int p = lab[x];
   while (p != x) {
+    const int gp = lab[p];
+    if (gp != p) lab[x] = gp;
     x = p;
-    p = lab[x];
+    p = gp;
   }
   return x;
 }
@@ -92,22 +96,23 @@ __global__ void __launch_bounds__(kCT) k_cc_union(int* __restrict__ lab, int nz,
   }
 }
 
-__global__ void __launch_bounds__(kCT) k_cc_flatten(int* __restrict__ lab, int* __restrict__ flag, int n) {
+// each voxel's root goes to `root` (the output buffer), not back into `lab`:
+// another thread's stale halving store could overwrite it there
+__global__ void __launch_bounds__(kCT)
+k_cc_flatten(int* __restrict__ lab, int* __restrict__ flag, int n, int* __restrict__ root) {
   for (int i = blockIdx.x * kCT + threadIdx.x; i < n; i += gridDim.x * kCT) {
     const int l = lab[i];
-    int root = -1;
-    if (l >= 0) root = cc_find(lab, i);
-    flag[i] = (l >= 0 && root == i) ? 1 : 0;
-    // roots are final after the union kernel: writing them back is safe
-    if (l >= 0) lab[i] = root;
+    const int r = l >= 0 ? cc_find(lab, i) : -1;
+    flag[i] = (l >= 0 && r == i) ? 1 : 0;
+    root[i] = r;
   }
 }
 
 __global__ void __launch_bounds__(kCT)
-k_cc_relabel(const int* __restrict__ lab, const int* __restrict__ ids, int n, uint32_t* __restrict__ out) {
+k_cc_relabel(const int* root, const int* __restrict__ ids, int n, uint32_t* out) {
   for (int i = blockIdx.x * kCT + threadIdx.x; i < n; i += gridDim.x * kCT) {
-    const int l = lab[i];
-    out[i] = l >= 0 ? (uint32_t)(ids[l] + 1) : 0u;
+    const int r = root[i];
+    out[i] = r >= 0 ? (uint32_t)(ids[r] + 1) : 0u;  // in place over root (same index)
   }
 }
 
@@ -133,11 +138,11 @@ cudaError_t connected_components(const void* in, int dt, int64_t nz, int64_t ny,
   }
   if (conn == 6) k_cc_union<6><<<g, kCT, 0, s>>>(lab, (int)nz, (int)ny, (int)nx);
   else k_cc_union<26><<<g, kCT, 0, s>>>(lab, (int)nz, (int)ny, (int)nx);
-  k_cc_flatten<<<g, kCT, 0, s>>>(lab, flag, n);
+  k_cc_flatten<<<g, kCT, 0, s>>>(lab, flag, n, reinterpret_cast<int*>(out));
   size_t need = scan_bytes;
   cudaError_t e = cub::DeviceScan::ExclusiveSum(scan_tmp, need, flag, ids, n, s);
   if (e != cudaSuccess) return e;
-  k_cc_relabel<<<g, kCT, 0, s>>>(lab, ids, n, out);
+  k_cc_relabel<<<g, kCT, 0, s>>>(reinterpret_cast<const int*>(out), ids, n, out);
   if (count) {
     int last_id = 0, last_flag = 0;
     cudaMemcpyAsync(&last_id, ids + n - 1, 4, cudaMemcpyDeviceToHost, s);
