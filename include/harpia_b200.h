@@ -207,6 +207,12 @@ int32_t hb_histogram(const hb_volume* in, int32_t device, int32_t bins, double l
  * device; any nonzero voxel is foreground. */
 int32_t hb_connected_components(const hb_volume* in, hb_volume* out, int32_t connectivity,
                                 int32_t device, int64_t* count);
+/* Label-volume filters built on the same labelling (out: the input's dtype and
+ * shape): op 0 = fill_holes (morphology.py:176-194: zero components not
+ * touching a volume face become 1), op 1 = remove_islands (morphology.py:
+ * 209-229: components of equal nonzero value smaller than min_size become 0). */
+int32_t hb_label_filter(const hb_volume* in, hb_volume* out, int32_t op, int32_t connectivity,
+                        int64_t min_size, int32_t device);
 
 /* Pinned-host helpers (cudaHostRegister for the duration of a job). */
 int32_t hb_pin(void* ptr, int64_t bytes);

@@ -30,10 +30,20 @@ inline int cgrid(int64_t n) {
   return (int)(b < 1 ? 1 : (b < cap ? b : cap));
 }
 
-template <typename T>
+// modes: CC_NONZERO (components of nonzero voxels), CC_ZERO (components of
+// the zero voxels: fill_holes' background), CC_SAME (nonzero voxels connect
+// only to equal values: remove_islands' per-label components)
+enum { CC_NONZERO = 0, CC_ZERO = 1, CC_SAME = 2 };
+
+template <typename T, int MODE>
+__device__ __forceinline__ bool cc_fg(T v) {
+  return MODE == CC_ZERO ? v == T(0) : v != T(0);
+}
+
+template <typename T, int MODE>
 __global__ void __launch_bounds__(kCT) k_cc_init(const T* __restrict__ in, int n, int* __restrict__ lab) {
   for (int i = blockIdx.x * kCT + threadIdx.x; i < n; i += gridDim.x * kCT)
-    lab[i] = in[i] != T(0) ? i : -1;
+    lab[i] = cc_fg<T, MODE>(in[i]) ? i : -1;
 }
 
 // find with path halving: a link is only ever rewritten while its node is a
@@ -68,16 +78,19 @@ __device__ __forceinline__ void cc_union(int* lab, int a, int b) {
   }
 }
 
-template <int CONN>
-__global__ void __launch_bounds__(kCT) k_cc_union(int* __restrict__ lab, int nz, int ny, int nx) {
+template <int CONN, typename T, int MODE>
+__global__ void __launch_bounds__(kCT)
+k_cc_union(int* __restrict__ lab, const T* __restrict__ in, int nz, int ny, int nx) {
   const int plane = ny * nx, n = nz * plane;
   for (int i = blockIdx.x * kCT + threadIdx.x; i < n; i += gridDim.x * kCT) {
     if (lab[i] < 0) continue;
     const int z = i / plane, r = i - z * plane, y = r / nx, x = r - y * nx;
+    const T vi = MODE == CC_SAME ? in[i] : T(0);
+    auto linked = [&](int j) { return lab[j] >= 0 && (MODE != CC_SAME || in[j] == vi); };
     if (CONN == 6) {
-      if (x > 0 && lab[i - 1] >= 0) cc_union(lab, i, i - 1);
-      if (y > 0 && lab[i - nx] >= 0) cc_union(lab, i, i - nx);
-      if (z > 0 && lab[i - plane] >= 0) cc_union(lab, i, i - plane);
+      if (x > 0 && linked(i - 1)) cc_union(lab, i, i - 1);
+      if (y > 0 && linked(i - nx)) cc_union(lab, i, i - nx);
+      if (z > 0 && linked(i - plane)) cc_union(lab, i, i - plane);
     } else {
       // the 13 neighbours that precede i in scan order
 #pragma unroll
@@ -90,7 +103,7 @@ __global__ void __launch_bounds__(kCT) k_cc_union(int* __restrict__ lab, int nz,
             const int zz = z + dz, yy = y + dy, xx = x + dx;
             if (zz < 0 || yy < 0 || yy >= ny || xx < 0 || xx >= nx) continue;
             const int j = i + dz * plane + dy * nx + dx;
-            if (lab[j] >= 0) cc_union(lab, i, j);
+            if (linked(j)) cc_union(lab, i, j);
           }
     }
   }
@@ -116,6 +129,70 @@ k_cc_relabel(const int* root, const int* __restrict__ ids, int n, uint32_t* out)
   }
 }
 
+// fill_holes: mark the roots of zero components that touch a volume face
+__global__ void __launch_bounds__(kCT)
+k_mark_border(const int* __restrict__ root, int nz, int ny, int nx, int* __restrict__ mark) {
+  const int plane = ny * nx, n = nz * plane;
+  for (int i = blockIdx.x * kCT + threadIdx.x; i < n; i += gridDim.x * kCT) {
+    const int r = root[i];
+    if (r < 0) continue;
+    const int z = i / plane, rr = i - z * plane, y = rr / nx, x = rr - y * nx;
+    if (z == 0 || z == nz - 1 || y == 0 || y == ny - 1 || x == 0 || x == nx - 1) mark[r] = 1;
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kCT)
+k_fill(const T* __restrict__ in, const int* __restrict__ root, const int* __restrict__ mark, int n,
+       T* __restrict__ out) {
+  for (int i = blockIdx.x * kCT + threadIdx.x; i < n; i += gridDim.x * kCT) {
+    const int r = root[i];
+    out[i] = (r >= 0 && !mark[r]) ? T(1) : in[i];
+  }
+}
+
+__global__ void __launch_bounds__(kCT) k_sizes(const int* __restrict__ root, int n, int* __restrict__ size) {
+  for (int i = blockIdx.x * kCT + threadIdx.x; i < n; i += gridDim.x * kCT) {
+    const int r = root[i];
+    if (r >= 0) atomicAdd(&size[r], 1);
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kCT)
+k_drop_small(const T* __restrict__ in, const int* __restrict__ root, const int* __restrict__ size,
+             int n, int64_t min_size, T* __restrict__ out) {
+  for (int i = blockIdx.x * kCT + threadIdx.x; i < n; i += gridDim.x * kCT) {
+    const int r = root[i];
+    out[i] = (r >= 0 && (int64_t)size[r] < min_size) ? T(0) : in[i];
+  }
+}
+
+// union-find labelling: root[i] = smallest index of i's component, -1 off it
+template <typename T, int MODE>
+void cc_label_t(const T* in, int nz, int ny, int nx, int conn, int* lab, int* root, int* flag,
+                cudaStream_t s) {
+  const int n = nz * ny * nx;
+  const int g = cgrid(n);
+  k_cc_init<T, MODE><<<g, kCT, 0, s>>>(in, n, lab);
+  if (conn == 6) k_cc_union<6, T, MODE><<<g, kCT, 0, s>>>(lab, in, nz, ny, nx);
+  else k_cc_union<26, T, MODE><<<g, kCT, 0, s>>>(lab, in, nz, ny, nx);
+  k_cc_flatten<<<g, kCT, 0, s>>>(lab, flag, n, root);
+}
+
+template <int MODE>
+cudaError_t cc_label(const void* in, int dt, int nz, int ny, int nx, int conn, int* lab, int* root,
+                     int* flag, cudaStream_t s) {
+  switch (dt) {
+    case HB_U8: cc_label_t<uint8_t, MODE>((const uint8_t*)in, nz, ny, nx, conn, lab, root, flag, s); break;
+    case HB_U16: cc_label_t<uint16_t, MODE>((const uint16_t*)in, nz, ny, nx, conn, lab, root, flag, s); break;
+    case HB_U32: cc_label_t<uint32_t, MODE>((const uint32_t*)in, nz, ny, nx, conn, lab, root, flag, s); break;
+    case HB_F32: cc_label_t<float, MODE>((const float*)in, nz, ny, nx, conn, lab, root, flag, s); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
 }  // namespace
 
 cudaError_t connected_components(const void* in, int dt, int64_t nz, int64_t ny, int64_t nx,
@@ -129,20 +206,13 @@ cudaError_t connected_components(const void* in, int dt, int64_t nz, int64_t ny,
   if (n64 >= (1ll << 31) - 1) return cudaErrorNotSupported;
   const int n = (int)n64;
   const int g = cgrid(n64);
-  switch (dt) {
-    case HB_U8: k_cc_init<uint8_t><<<g, kCT, 0, s>>>((const uint8_t*)in, n, lab); break;
-    case HB_U16: k_cc_init<uint16_t><<<g, kCT, 0, s>>>((const uint16_t*)in, n, lab); break;
-    case HB_U32: k_cc_init<uint32_t><<<g, kCT, 0, s>>>((const uint32_t*)in, n, lab); break;
-    case HB_F32: k_cc_init<float><<<g, kCT, 0, s>>>((const float*)in, n, lab); break;
-    default: return cudaErrorInvalidValue;
-  }
-  if (conn == 6) k_cc_union<6><<<g, kCT, 0, s>>>(lab, (int)nz, (int)ny, (int)nx);
-  else k_cc_union<26><<<g, kCT, 0, s>>>(lab, (int)nz, (int)ny, (int)nx);
-  k_cc_flatten<<<g, kCT, 0, s>>>(lab, flag, n, reinterpret_cast<int*>(out));
-  size_t need = scan_bytes;
-  cudaError_t e = cub::DeviceScan::ExclusiveSum(scan_tmp, need, flag, ids, n, s);
+  int* root = reinterpret_cast<int*>(out);  // roots first, compacted ids in place after
+  cudaError_t e = cc_label<CC_NONZERO>(in, dt, (int)nz, (int)ny, (int)nx, conn, lab, root, flag, s);
   if (e != cudaSuccess) return e;
-  k_cc_relabel<<<g, kCT, 0, s>>>(reinterpret_cast<const int*>(out), ids, n, out);
+  size_t need = scan_bytes;
+  e = cub::DeviceScan::ExclusiveSum(scan_tmp, need, flag, ids, n, s);
+  if (e != cudaSuccess) return e;
+  k_cc_relabel<<<g, kCT, 0, s>>>(root, ids, n, out);
   if (count) {
     int last_id = 0, last_flag = 0;
     cudaMemcpyAsync(&last_id, ids + n - 1, 4, cudaMemcpyDeviceToHost, s);
@@ -150,6 +220,35 @@ cudaError_t connected_components(const void* in, int dt, int64_t nz, int64_t ny,
     e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) return e;
     *count = (int64_t)last_id + last_flag;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t label_filter(const void* in, int dt, int64_t nz, int64_t ny, int64_t nx, int conn,
+                         int op, int64_t min_size, void* out, int* lab, int* root, int* aux,
+                         cudaStream_t s) {
+  const int64_t n64 = nz * ny * nx;
+  if (n64 <= 0) return cudaSuccess;
+  if (n64 >= (1ll << 31) - 1) return cudaErrorNotSupported;
+  const int n = (int)n64;
+  const int g = cgrid(n64);
+  cudaError_t e = op == 0 ? cc_label<CC_ZERO>(in, dt, (int)nz, (int)ny, (int)nx, conn, lab, root, aux, s)
+                          : cc_label<CC_SAME>(in, dt, (int)nz, (int)ny, (int)nx, conn, lab, root, aux, s);
+  if (e != cudaSuccess) return e;
+  cudaMemsetAsync(aux, 0, (size_t)n * 4, s);  // border marks / component sizes, by root
+  if (op == 0) k_mark_border<<<g, kCT, 0, s>>>(root, (int)nz, (int)ny, (int)nx, aux);
+  else k_sizes<<<g, kCT, 0, s>>>(root, n, aux);
+  switch (dt) {
+#define HB_LF(T)                                                                                  \
+  if (op == 0) k_fill<T><<<g, kCT, 0, s>>>((const T*)in, root, aux, n, (T*)out);                  \
+  else k_drop_small<T><<<g, kCT, 0, s>>>((const T*)in, root, aux, n, min_size, (T*)out);          \
+  break;
+    case HB_U8: HB_LF(uint8_t)
+    case HB_U16: HB_LF(uint16_t)
+    case HB_U32: HB_LF(uint32_t)
+    case HB_F32: HB_LF(float)
+#undef HB_LF
+    default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
 }

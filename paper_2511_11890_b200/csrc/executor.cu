@@ -855,6 +855,75 @@ int32_t hb_connected_components(const hb_volume* in, hb_volume* out, int32_t con
   return HB_OK;
 }
 
+int32_t hb_label_filter(const hb_volume* in, hb_volume* out, int32_t op, int32_t connectivity,
+                        int64_t min_size, int32_t device) {
+  if (!in || !out || !in->data || !out->data || out->dtype != in->dtype || in->nz != out->nz ||
+      in->ny != out->ny || in->nx != out->nx || (op != 0 && op != 1)) {
+    set_err(nullptr, "hb_label_filter: op 0/1 and an output of the input's dtype and shape");
+    return HB_EPARAM;
+  }
+  if (connectivity != 6 && connectivity != 26) {
+    set_err(nullptr, "connectivity must be 6 or 26, got " + std::to_string(connectivity));
+    return HB_EPARAM;
+  }
+  if (op == 1 && min_size < 1) {
+    set_err(nullptr, "min_size must be >= 1, got " + std::to_string(min_size));
+    return HB_EPARAM;
+  }
+  if (device < 0 || device >= hb_device_count()) {
+    set_err(nullptr, "no CUDA device " + std::to_string(device));
+    return HB_EBUDGET_UNAVAILABLE;
+  }
+  const int64_t n = in->nz * in->ny * in->nx;
+  if (n >= (1ll << 31) - 1) {
+    set_err(nullptr, "label filters: volumes of 2^31 voxels or more are not supported");
+    return HB_EUNSUPPORTED;
+  }
+  std::lock_guard<std::mutex> lk(g_dev[device].mu);
+  cudaSetDevice(device);
+  cudaError_t e = ensure_pool(device);
+  if (e != cudaSuccess) {
+    set_err(nullptr, cudaGetErrorString(e));
+    return HB_ECUDA;
+  }
+  cudaStream_t s;
+  cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+  PoolAlloc pa{g_dev[device].pool, s};
+  const size_t es = (size_t)dtype_size(in->dtype), nn = (size_t)std::max<int64_t>(n, 1);
+  int* lab = (int*)pa.get(nn * 4);
+  int* root = (int*)pa.get(nn * 4);
+  int* aux = (int*)pa.get(nn * 4);
+  const void* d_in = in->data;
+  void* d_out = out->data;
+  if (in->location != HB_DEVICE && aux) {
+    void* buf = pa.get(nn * es);
+    if (buf) {
+      e = cudaMemcpyAsync(buf, in->data, (size_t)n * es, cudaMemcpyHostToDevice, s);
+      d_in = buf;
+    }
+  }
+  if (out->location != HB_DEVICE && aux) d_out = pa.get(nn * es);
+  if (!lab || !root || !aux || !d_out || pa.err != cudaSuccess)
+    e = pa.err != cudaSuccess ? pa.err : cudaErrorMemoryAllocation;
+  if (e == cudaSuccess)
+    e = label_filter(d_in, in->dtype, in->nz, in->ny, in->nx, connectivity, op, min_size, d_out,
+                     lab, root, aux, s);
+  if (e == cudaSuccess && out->location != HB_DEVICE)
+    e = cudaMemcpyAsync(out->data, d_out, (size_t)n * es, cudaMemcpyDeviceToHost, s);
+  cudaError_t se = cudaStreamSynchronize(s);
+  if (e == cudaSuccess) e = se;
+  pa.release();
+  cudaStreamSynchronize(s);
+  cudaStreamDestroy(s);
+  if (g_dev[device].session.load() == 0) cudaMemPoolTrimTo(g_dev[device].pool, 0);
+  if (e != cudaSuccess) {
+    set_err(nullptr, std::string("label filter: ") + cudaGetErrorString(e));
+    cudaGetLastError();
+    return e == cudaErrorMemoryAllocation ? HB_EBUDGET_UNAVAILABLE : HB_ECUDA;
+  }
+  return HB_OK;
+}
+
 int32_t hb_histogram(const hb_volume* in, int32_t device, int32_t bins, double lo, double hi,
                      const double* edges, int32_t edges_f32, int64_t* counts) {
   if (!in || bins < 1 || !edges || !counts || !(hi > lo) || !std::isfinite(lo) || !std::isfinite(hi)) {

@@ -112,6 +112,10 @@ cudaError_t connected_components(const void* in, int dt, int64_t nz, int64_t ny,
                                  int conn, uint32_t* out, int* lab, int* flag, int* ids,
                                  void* scan_tmp, size_t scan_bytes, int64_t* count, cudaStream_t s);
 size_t connected_components_scan_bytes(int64_t n);
+// op 0 fill_holes, op 1 remove_islands; lab/root/aux: n ints each
+cudaError_t label_filter(const void* in, int dt, int64_t nz, int64_t ny, int64_t nx, int conn,
+                         int op, int64_t min_size, void* out, int* lab, int* root, int* aux,
+                         cudaStream_t s);
 
 // --- median (median.cu) ----------------------------------------------------
 cudaError_t median(const DevIn& in, int64_t zo, int64_t nzo, void* out, int r,

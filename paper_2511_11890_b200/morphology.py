@@ -129,3 +129,50 @@ def morph(data, op: str, se: StructuringElement, iterations: int = 1):
     from .filters import apply_program
 
     return apply_program(data, morph_program(op, se, iterations))
+
+
+# ---------------------------------------------------------------------------
+# Label-volume filters (global operators) on the device labelling (cc.cu)
+# ---------------------------------------------------------------------------
+def _label_filter(data, op: int, connectivity: int, min_size: int = 0):
+    import ctypes
+
+    from . import _native
+
+    if connectivity not in (6, 26):
+        raise ParameterError(f"connectivity must be 6 or 26, got {connectivity}")
+    L = _native.load()
+    if hasattr(data, "data_ptr"):
+        import torch
+
+        x = data.contiguous()
+        out = torch.empty_like(x)
+    else:
+        x = np.asarray(data)
+        if x.ndim != 3:
+            raise ParameterError(f"expected a 3D (Z, Y, X) volume, got shape {x.shape}")
+        if x.dtype not in _native.DTYPE_CODE:
+            raise ParameterError(f"label filters need uint8/16/32 or float32 data, got {x.dtype}")
+        x = np.ascontiguousarray(x)
+        out = np.empty_like(x)
+    vin, _ = _native._volume_of(x)
+    vout, _ = _native._volume_of(out)
+    rc = L.hb_label_filter(ctypes.byref(vin), ctypes.byref(vout), op, int(connectivity),
+                           int(min_size), _native.current_device())
+    _native.raise_for_status(rc, _native.last_error())
+    return out
+
+
+def fill_holes(mask, connectivity: int = 6):
+    """Fill the zero components that do not touch a volume face with 1
+    (morphology.py:176-194); dtype preserved."""
+    return _label_filter(mask, 0, connectivity)
+
+
+def remove_islands(data, min_size: int, connectivity: int = 6):
+    """Zero the components smaller than ``min_size`` voxels; voxels connect
+    only to equal nonzero values, so touching labels stay separate
+    (morphology.py:209-229)."""
+    if min_size < 1:
+        raise ParameterError(f"min_size must be >= 1, got {min_size}")
+    return _label_filter(data, 1, connectivity, min_size)

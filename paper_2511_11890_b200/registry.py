@@ -258,6 +258,29 @@ def _run_cc(data, params, budget, cancel):
 register(Operator(name="connected_components", kind="global", output="labels",
                   schema={"connectivity": (int, 6)}, run=_run_cc))
 
+
+# label-volume filters (registry.py:355-383) on the device labelling
+def _run_fill_holes(data, params, budget, cancel):
+    from .ledger import LEDGER
+
+    LEDGER.job_start()
+    return morphology.fill_holes(data, params["connectivity"]), ExecutionReport(chunk_count=1)
+
+
+def _run_remove_islands(data, params, budget, cancel):
+    from .ledger import LEDGER
+
+    LEDGER.job_start()
+    out = morphology.remove_islands(data, params["min_size"], params["connectivity"])
+    return out, ExecutionReport(chunk_count=1)
+
+
+register(Operator(name="fill_holes", kind="global", output="labels",
+                  schema={"connectivity": (int, 6)}, run=_run_fill_holes, label_input=True))
+register(Operator(name="remove_islands", kind="global", output="labels",
+                  schema={"min_size": (int, REQUIRED), "connectivity": (int, 6)},
+                  run=_run_remove_islands, label_input=True))
+
 # LoG = hessian trace; profile as the reference's hessian_* (registry.py:234-246)
 _map("log",
      {"sigma": (float, REQUIRED), "precision": (_precision_param, "exact")},

@@ -93,6 +93,22 @@ def main():
         for conn in (6, 26):
             lab, _n = Q.connected_components(vols[vol], conn)
             add(f"cc_{vol}_{conn}", "connected_components", {"connectivity": conn}, vol, lab)
+    # label-volume filters (registry.py:355-383)
+    rl = np.random.default_rng(77)
+    labvol = rl.integers(0, 4, size=(14, 17, 19)).astype(np.uint32)
+    labvol[rl.random(labvol.shape) < 0.3] = 0
+    arrays["in__lab_a"] = labvol
+    holes = (rl.random((13, 16, 18)) < 0.55).astype(np.uint8)
+    arrays["in__holes_a"] = holes
+    for vol in ("lab_a", "holes_a", "bin_a"):
+        src = arrays[f"in__{vol}"]
+        for conn in (6, 26):
+            add(f"fill_holes_{vol}_{conn}", "fill_holes", {"connectivity": conn}, vol,
+                ref.morphology.fill_holes(src, conn).astype(src.dtype))
+            for ms in (1, 3, 9):
+                add(f"remove_islands_{vol}_{conn}_{ms}", "remove_islands",
+                    {"min_size": ms, "connectivity": conn}, vol,
+                    ref.morphology.remove_islands(src, ms, conn))
     # global Otsu (registry.py:312-334): binarized output; threshold in meta
     otsu_t = {}
     for vol in ("f32_a", "f32_unit", "u8_a", "u16_a", "f32_neg", "bin_a"):

@@ -432,3 +432,25 @@ def test_connected_components_vs_oracle(hb, oracle, conn):
     lab, rep = registry.run_operator(m.astype(np.uint8), "connected_components", {"connectivity": conn},
                                      budget_for(OpProfile(0, 6), m.shape, np.uint8, 4))
     assert rep.component_count == n and np.array_equal(lab, want)
+
+
+def test_label_filters_vs_oracle(hb, oracle):
+    """fill_holes / remove_islands (morphology.py:176-229) on the device
+    labelling: bit-exact, dtype preserved, host and device inputs."""
+    import torch
+
+    from paper_2511_11890_b200 import morphology
+
+    rng = np.random.default_rng(21)
+    for shape in ((24, 40, 33), (5, 1, 60), (40, 40, 40)):
+        m = (rng.random(shape) < 0.6).astype(np.uint8)
+        lab = rng.integers(0, 5, size=shape).astype(np.uint32)
+        lab[rng.random(shape) < 0.35] = 0
+        for conn in (6, 26):
+            assert np.array_equal(morphology.fill_holes(m, conn), oracle.fill_holes(m, conn))
+            assert np.array_equal(morphology.fill_holes(lab, conn), oracle.fill_holes(lab, conn))
+            for ms in (2, 6):
+                got = morphology.remove_islands(lab, ms, conn)
+                assert got.dtype == lab.dtype and np.array_equal(got, oracle.remove_islands(lab, ms, conn))
+    dev = morphology.remove_islands(torch.from_numpy(lab).cuda(), 4, 26)
+    assert np.array_equal(dev.cpu().numpy(), oracle.remove_islands(lab, 4, 26))
