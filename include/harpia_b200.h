@@ -213,6 +213,13 @@ int32_t hb_connected_components(const hb_volume* in, hb_volume* out, int32_t con
  * 209-229: components of equal nonzero value smaller than min_size become 0). */
 int32_t hb_label_filter(const hb_volume* in, hb_volume* out, int32_t op, int32_t connectivity,
                         int64_t min_size, int32_t device);
+/* Geodesic reconstruction (morphology.py:143-165): fixed point of
+ * min(dilate(m, cross(1)), mask) (dilation = 1) or max(erode(m, cross(1)),
+ * mask) (dilation = 0) from `marker`; marker, mask and out share dtype and
+ * shape; EPARAM if marker > mask (dilation) / marker < mask (erosion)
+ * anywhere.  `sweeps` (optional) receives the number of in-place passes. */
+int32_t hb_geodesic(const hb_volume* marker, const hb_volume* mask, hb_volume* out,
+                    int32_t dilation, int32_t device, int64_t* sweeps);
 
 /* Pinned-host helpers (cudaHostRegister for the duration of a job). */
 int32_t hb_pin(void* ptr, int64_t bytes);

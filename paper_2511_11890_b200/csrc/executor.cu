@@ -924,6 +924,69 @@ int32_t hb_label_filter(const hb_volume* in, hb_volume* out, int32_t op, int32_t
   return HB_OK;
 }
 
+int32_t hb_geodesic(const hb_volume* marker, const hb_volume* mask, hb_volume* out,
+                    int32_t dilation, int32_t device, int64_t* sweeps) {
+  if (!marker || !mask || !out || !marker->data || !mask->data || !out->data ||
+      marker->dtype != mask->dtype || out->dtype != mask->dtype || marker->nz != mask->nz ||
+      marker->ny != mask->ny || marker->nx != mask->nx || out->nz != mask->nz ||
+      out->ny != mask->ny || out->nx != mask->nx) {
+    set_err(nullptr, "hb_geodesic: marker, mask and out must share dtype and shape");
+    return HB_EPARAM;
+  }
+  if (device < 0 || device >= hb_device_count()) {
+    set_err(nullptr, "no CUDA device " + std::to_string(device));
+    return HB_EBUDGET_UNAVAILABLE;
+  }
+  std::lock_guard<std::mutex> lk(g_dev[device].mu);
+  cudaSetDevice(device);
+  cudaError_t e = ensure_pool(device);
+  if (e != cudaSuccess) {
+    set_err(nullptr, cudaGetErrorString(e));
+    return HB_ECUDA;
+  }
+  const int64_t n = mask->nz * mask->ny * mask->nx;
+  const size_t es = (size_t)dtype_size(mask->dtype), nn = (size_t)std::max<int64_t>(n, 1);
+  cudaStream_t s;
+  cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+  PoolAlloc pa{g_dev[device].pool, s};
+  int* flags = (int*)pa.get(64);
+  auto dev_copy = [&](const hb_volume* v) -> const void* {
+    if (v->location == HB_DEVICE) return v->data;
+    void* b = pa.get(nn * es);
+    if (b && e == cudaSuccess) e = cudaMemcpyAsync(b, v->data, (size_t)n * es, cudaMemcpyHostToDevice, s);
+    return b;
+  };
+  const void* d_marker = dev_copy(marker);
+  const void* d_mask = dev_copy(mask);
+  void* d_out = out->location == HB_DEVICE ? out->data : pa.get(nn * es);
+  if (!flags || !d_marker || !d_mask || !d_out || pa.err != cudaSuccess)
+    e = pa.err != cudaSuccess ? pa.err : cudaErrorMemoryAllocation;
+  int64_t k = 0;
+  if (e == cudaSuccess)
+    e = geodesic(d_marker, d_mask, mask->dtype, mask->nz, mask->ny, mask->nx, dilation != 0, d_out,
+                 flags, s, &k);
+  const bool order_bad = e == cudaErrorInvalidValue;
+  if (e == cudaSuccess && out->location != HB_DEVICE)
+    e = cudaMemcpyAsync(out->data, d_out, (size_t)n * es, cudaMemcpyDeviceToHost, s);
+  cudaStreamSynchronize(s);
+  pa.release();
+  cudaStreamSynchronize(s);
+  cudaStreamDestroy(s);
+  if (g_dev[device].session.load() == 0) cudaMemPoolTrimTo(g_dev[device].pool, 0);
+  cudaGetLastError();
+  if (order_bad) {
+    set_err(nullptr, dilation ? "reconstruction by dilation requires marker <= mask"
+                              : "reconstruction by erosion requires marker >= mask");
+    return HB_EPARAM;
+  }
+  if (e != cudaSuccess) {
+    set_err(nullptr, std::string("geodesic reconstruction: ") + cudaGetErrorString(e));
+    return e == cudaErrorMemoryAllocation ? HB_EBUDGET_UNAVAILABLE : HB_ECUDA;
+  }
+  if (sweeps) *sweeps = k;
+  return HB_OK;
+}
+
 int32_t hb_histogram(const hb_volume* in, int32_t device, int32_t bins, double lo, double hi,
                      const double* edges, int32_t edges_f32, int64_t* counts) {
   if (!in || bins < 1 || !edges || !counts || !(hi > lo) || !std::isfinite(lo) || !std::isfinite(hi)) {

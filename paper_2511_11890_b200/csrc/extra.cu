@@ -277,3 +277,103 @@ cudaError_t threshold(const DevIn& in, int64_t zo, int64_t nzo, uint32_t* out, d
 }
 
 }  // namespace hb
+
+// ---------------------------------------------------------------------------
+// geodesic reconstruction (morphology.py:143-165): the fixed point of
+// m <- min(dilate(m, cross(1)), mask) (or max(erode(m, cross(1)), mask)).  The
+// reconstruction is the unique fixed point of this monotone map, so in-place
+// (chaotic) sweeps reach exactly the reference's Jacobi result, in fewer
+// passes; sweeps repeat until one changes nothing.
+// ---------------------------------------------------------------------------
+namespace hb {
+namespace {
+
+template <typename T, bool DIL>
+__global__ void __launch_bounds__(kT)
+k_geo_check(const T* __restrict__ marker, const T* __restrict__ mask, int64_t n, int* __restrict__ bad) {
+  for (int64_t i = blockIdx.x * (int64_t)kT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kT) {
+    const T a = marker[i], b = mask[i];
+    if (DIL ? a > b : a < b) {
+      *bad = 1;
+      return;
+    }
+  }
+}
+
+template <typename T, bool DIL>
+__global__ void __launch_bounds__(kT)
+k_geo_sweep(T* cur, const T* __restrict__ mask, int nz, int ny, int nx, int* __restrict__ changed) {
+  const int64_t plane = (int64_t)ny * nx, n = (int64_t)nz * plane;
+  bool any = false;
+  for (int64_t i = blockIdx.x * (int64_t)kT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kT) {
+    const int z = (int)(i / plane);
+    const int64_t rr = i - (int64_t)z * plane;
+    const int y = (int)(rr / nx), x = (int)(rr % nx);
+    const T v = cur[i];
+    T m = v;
+    auto take = [&](int64_t j) {
+      const T u = *((volatile const T*)(cur + j));
+      m = DIL ? (u > m ? u : m) : (u < m ? u : m);
+    };
+    if (x > 0) take(i - 1);
+    if (x < nx - 1) take(i + 1);
+    if (y > 0) take(i - nx);
+    if (y < ny - 1) take(i + nx);
+    if (z > 0) take(i - plane);
+    if (z < nz - 1) take(i + plane);
+    const T b = mask[i];
+    const T nv = DIL ? (m < b ? m : b) : (m > b ? m : b);
+    if (nv != v) {
+      cur[i] = nv;
+      any = true;
+    }
+  }
+  if (any) *changed = 1;
+}
+
+template <typename T, bool DIL>
+cudaError_t geo_t(const T* marker, const T* mask, int64_t nz, int64_t ny, int64_t nx, T* out,
+                  int* flags, cudaStream_t s, int64_t* sweeps) {
+  const int64_t n = nz * ny * nx;
+  const int g = grid_for(n);
+  int h = 0;
+  cudaMemsetAsync(flags, 0, 4, s);
+  k_geo_check<T, DIL><<<g, kT, 0, s>>>(marker, mask, n, flags);
+  cudaMemcpyAsync(&h, flags, 4, cudaMemcpyDeviceToHost, s);
+  cudaError_t e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return e;
+  if (h) return cudaErrorInvalidValue;  // marker violates the ordering
+  if ((const void*)out != (const void*)marker)
+    cudaMemcpyAsync(out, marker, (size_t)n * sizeof(T), cudaMemcpyDeviceToDevice, s);
+  int64_t k = 0;
+  do {
+    cudaMemsetAsync(flags, 0, 4, s);
+    k_geo_sweep<T, DIL><<<g, kT, 0, s>>>(out, mask, (int)nz, (int)ny, (int)nx, flags);
+    cudaMemcpyAsync(&h, flags, 4, cudaMemcpyDeviceToHost, s);
+    e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return e;
+    ++k;
+  } while (h);
+  if (sweeps) *sweeps = k;
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t geodesic(const void* marker, const void* mask, int dt, int64_t nz, int64_t ny, int64_t nx,
+                     bool dilation, void* out, int* flags, cudaStream_t s, int64_t* sweeps) {
+  if (nz * ny * nx <= 0) return cudaSuccess;
+#define HB_GEO(T)                                                                                     \
+  return dilation ? geo_t<T, true>((const T*)marker, (const T*)mask, nz, ny, nx, (T*)out, flags, s, sweeps) \
+                  : geo_t<T, false>((const T*)marker, (const T*)mask, nz, ny, nx, (T*)out, flags, s, sweeps);
+  switch (dt) {
+    case HB_U8: HB_GEO(uint8_t)
+    case HB_U16: HB_GEO(uint16_t)
+    case HB_U32: HB_GEO(uint32_t)
+    case HB_F32: HB_GEO(float)
+  }
+#undef HB_GEO
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace hb

@@ -112,6 +112,9 @@ cudaError_t connected_components(const void* in, int dt, int64_t nz, int64_t ny,
                                  int conn, uint32_t* out, int* lab, int* flag, int* ids,
                                  void* scan_tmp, size_t scan_bytes, int64_t* count, cudaStream_t s);
 size_t connected_components_scan_bytes(int64_t n);
+// geodesic reconstruction (extra.cu); cudaErrorInvalidValue = marker ordering violated
+cudaError_t geodesic(const void* marker, const void* mask, int dt, int64_t nz, int64_t ny, int64_t nx,
+                     bool dilation, void* out, int* flags, cudaStream_t s, int64_t* sweeps);
 // op 0 fill_holes, op 1 remove_islands; lab/root/aux: n ints each
 cudaError_t label_filter(const void* in, int dt, int64_t nz, int64_t ny, int64_t nx, int conn,
                          int op, int64_t min_size, void* out, int* lab, int* root, int* aux,

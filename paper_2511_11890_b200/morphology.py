@@ -176,3 +176,35 @@ def remove_islands(data, min_size: int, connectivity: int = 6):
     if min_size < 1:
         raise ParameterError(f"min_size must be >= 1, got {min_size}")
     return _label_filter(data, 1, connectivity, min_size)
+
+
+def geodesic_reconstruct(marker, mask, kind: str = "dilation"):
+    """Reconstruction by iterated geodesic steps until the fixed point
+    (morphology.py:143-165): dilation: marker <= mask, step =
+    min(dilate(m, cross(1)), mask); erosion: marker >= mask, step =
+    max(erode(m, cross(1)), mask).  On the device with in-place sweeps (same
+    unique fixed point)."""
+    import ctypes
+
+    from . import _native
+
+    if kind not in ("dilation", "erosion"):
+        raise ParameterError(f"kind must be dilation or erosion, got {kind!r}")
+    mk, ms = np.asarray(marker), np.asarray(mask)
+    if mk.shape != ms.shape or ms.ndim != 3:
+        raise ParameterError("marker and mask must be 3D volumes of the same shape")
+    dt = np.result_type(mk, ms)  # np.minimum/np.maximum promote
+    if dt not in _native.DTYPE_CODE:
+        raise ParameterError(f"geodesic reconstruction needs uint8/16/32 or float32 data, got {dt}")
+    mk = np.ascontiguousarray(mk, dtype=dt)
+    ms = np.ascontiguousarray(ms, dtype=dt)
+    out = np.empty_like(ms)
+    vm, _ = _native._volume_of(mk)
+    vk, _ = _native._volume_of(ms)
+    vo, _ = _native._volume_of(out)
+    sweeps = ctypes.c_int64()
+    rc = _native.load().hb_geodesic(ctypes.byref(vm), ctypes.byref(vk), ctypes.byref(vo),
+                                    1 if kind == "dilation" else 0, _native.current_device(),
+                                    ctypes.byref(sweeps))
+    _native.raise_for_status(rc, _native.last_error())
+    return out

@@ -275,6 +275,18 @@ def _run_remove_islands(data, params, budget, cancel):
     return out, ExecutionReport(chunk_count=1)
 
 
+def _run_geodesic(data, params, budget, cancel):
+    from .ledger import LEDGER
+
+    LEDGER.job_start()
+    # whole-volume fixed point: the propagation range is unbounded (no halo)
+    out = morphology.geodesic_reconstruct(params["marker"], data, params["kind"])
+    return out, ExecutionReport(chunk_count=1)
+
+
+register(Operator(name="geodesic_reconstruct", kind="global", output="volume",
+                  schema={"marker": (np.asarray, REQUIRED), "kind": (str, "dilation")},
+                  run=_run_geodesic, label_input=True))
 register(Operator(name="fill_holes", kind="global", output="labels",
                   schema={"connectivity": (int, 6)}, run=_run_fill_holes, label_input=True))
 register(Operator(name="remove_islands", kind="global", output="labels",

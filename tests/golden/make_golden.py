@@ -109,6 +109,18 @@ def main():
                 add(f"remove_islands_{vol}_{conn}_{ms}", "remove_islands",
                     {"min_size": ms, "connectivity": conn}, vol,
                     ref.morphology.remove_islands(src, ms, conn))
+    # geodesic reconstruction (registry.py:386-401): marker in params (array key)
+    for vol, kind in (("u8_a", "dilation"), ("u16_a", "erosion"), ("f32_unit", "dilation")):
+        src = arrays[f"in__{vol}"]
+        if kind == "dilation":
+            marker = np.where(rl.random(src.shape) < 0.02, src, np.zeros_like(src)).astype(src.dtype)
+        else:
+            top = np.iinfo(src.dtype).max if src.dtype.kind == "u" else src.max()
+            marker = np.where(rl.random(src.shape) < 0.02, src, np.full_like(src, top)).astype(src.dtype)
+        arrays[f"marker__{vol}_{kind}"] = marker
+        add(f"geodesic_{vol}_{kind}", "geodesic_reconstruct",
+            {"marker": f"marker__{vol}_{kind}", "kind": kind}, vol,
+            ref.morphology.geodesic_reconstruct(marker, src, kind))
     # global Otsu (registry.py:312-334): binarized output; threshold in meta
     otsu_t = {}
     for vol in ("f32_a", "f32_unit", "u8_a", "u16_a", "f32_neg", "bin_a"):

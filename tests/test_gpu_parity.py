@@ -35,6 +35,8 @@ def _ours(hb, case, arrays, precision=None):
         return morphology.dilate(x, morphology.StructuringElement(tuple(map(tuple, arrays[p["offsets"]]))))
     if precision is not None and op in ("gaussian", "unsharp", "log"):
         p["precision"] = precision
+    if op == "geodesic_reconstruct":  # the marker travels as an array key
+        p["marker"] = arrays[p["marker"]]
     return registry.run_direct(x, op, p)
 
 
@@ -454,3 +456,24 @@ def test_label_filters_vs_oracle(hb, oracle):
                 assert got.dtype == lab.dtype and np.array_equal(got, oracle.remove_islands(lab, ms, conn))
     dev = morphology.remove_islands(torch.from_numpy(lab).cuda(), 4, 26)
     assert np.array_equal(dev.cpu().numpy(), oracle.remove_islands(lab, 4, 26))
+
+
+def test_geodesic_reconstruct_vs_oracle(hb, oracle):
+    """morphology.py:143-165: the device's in-place sweeps reach the same
+    (unique) fixed point as the reference's Jacobi steps; ordering violations
+    raise ParameterError."""
+    from paper_2511_11890_b200 import morphology
+    from paper_2511_11890_b200.errors import ParameterError
+
+    rng = np.random.default_rng(31)
+    for shape, dt in (((20, 30, 41), np.uint8), ((9, 64, 64), np.uint16), ((12, 1, 90), np.float32)):
+        mask = (rng.random(shape) * 200).astype(dt)
+        seeds = rng.random(shape) < 0.01
+        m_dil = np.where(seeds, mask, 0).astype(dt)
+        assert np.array_equal(morphology.geodesic_reconstruct(m_dil, mask, "dilation"),
+                              oracle.geodesic_reconstruct(m_dil, mask, "dilation"))
+        m_ero = np.where(seeds, mask, mask.max()).astype(dt)
+        assert np.array_equal(morphology.geodesic_reconstruct(m_ero, mask, "erosion"),
+                              oracle.geodesic_reconstruct(m_ero, mask, "erosion"))
+    with pytest.raises(ParameterError):
+        morphology.geodesic_reconstruct(mask.max() + np.zeros_like(mask) + 1, mask, "dilation")

@@ -16,6 +16,8 @@ def _run_case(O, case, arrays):
         return O.dilate(x, arrays[p["offsets"]])
     if op.startswith("morph_"):
         return O.morph(x, op[6:], O.parse_se(p["se"]), p.get("iterations", 1))
+    if op == "geodesic_reconstruct":  # the marker travels as an array key
+        p = dict(p, marker=arrays[p["marker"]])
     return O.apply(op, x, p)
 
 
