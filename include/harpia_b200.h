@@ -220,6 +220,11 @@ int32_t hb_label_filter(const hb_volume* in, hb_volume* out, int32_t op, int32_t
  * anywhere.  `sweeps` (optional) receives the number of in-place passes. */
 int32_t hb_geodesic(const hb_volume* marker, const hb_volume* mask, hb_volume* out,
                     int32_t dilation, int32_t device, int64_t* sweeps);
+/* Exact Euclidean distance transform (quantify.py:115-175): distance of every
+ * nonzero voxel to the nearest zero voxel with per-axis `spacing` (z, y, x).
+ * out dtype HB_F32: sqrt(d^2) cast to float32 (the reference's default);
+ * out dtype 4 (float64, squared=True): d^2.  No zero voxel -> +inf. */
+int32_t hb_edt(const hb_volume* in, hb_volume* out, const double* spacing, int32_t device);
 
 /* Pinned-host helpers (cudaHostRegister for the duration of a job). */
 int32_t hb_pin(void* ptr, int64_t bytes);

@@ -112,7 +112,7 @@ EXPORTS = (
     "hb_apply_device", "hb_chain_out_dtype", "hb_trim_device",
     "hb_device_pool_bytes", "hb_pin", "hb_unpin", "hb_last_error",
     "hb_session_begin", "hb_session_end", "hb_minmax", "hb_histogram",
-    "hb_connected_components", "hb_label_filter", "hb_geodesic",
+    "hb_connected_components", "hb_label_filter", "hb_geodesic", "hb_edt",
 )
 
 _lock = threading.Lock()
@@ -176,6 +176,8 @@ def load() -> ctypes.CDLL:
         L.hb_geodesic.argtypes = [ctypes.POINTER(HbVolume), ctypes.POINTER(HbVolume),
                                   ctypes.POINTER(HbVolume), i32, i32, ctypes.POINTER(ctypes.c_int64)]
         L.hb_geodesic.restype = i32
+        L.hb_edt.argtypes = [ctypes.POINTER(HbVolume), ctypes.POINTER(HbVolume), vp, i32]
+        L.hb_edt.restype = i32
         L.hb_pin.argtypes = [vp, i64]
         L.hb_pin.restype = i32
         L.hb_unpin.argtypes = [vp]

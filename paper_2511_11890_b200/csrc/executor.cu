@@ -987,6 +987,65 @@ int32_t hb_geodesic(const hb_volume* marker, const hb_volume* mask, hb_volume* o
   return HB_OK;
 }
 
+int32_t hb_edt(const hb_volume* in, hb_volume* out, const double* spacing, int32_t device) {
+  const int kF64 = 4;
+  if (!in || !out || !in->data || !out->data || !spacing || (out->dtype != HB_F32 && out->dtype != kF64) ||
+      in->nz != out->nz || in->ny != out->ny || in->nx != out->nx || in->dtype < HB_U8 || in->dtype > HB_F32) {
+    set_err(nullptr, "hb_edt: float32 (or float64 squared) output of the input's shape required");
+    return HB_EPARAM;
+  }
+  if (in->nz >= (1 << 30) || in->ny >= (1 << 30) || in->nx >= (1 << 30)) {
+    set_err(nullptr, "hb_edt: axis too long");
+    return HB_EUNSUPPORTED;
+  }
+  if (device < 0 || device >= hb_device_count()) {
+    set_err(nullptr, "no CUDA device " + std::to_string(device));
+    return HB_EBUDGET_UNAVAILABLE;
+  }
+  std::lock_guard<std::mutex> lk(g_dev[device].mu);
+  cudaSetDevice(device);
+  cudaError_t e = ensure_pool(device);
+  if (e != cudaSuccess) {
+    set_err(nullptr, cudaGetErrorString(e));
+    return HB_ECUDA;
+  }
+  const int64_t n = in->nz * in->ny * in->nx;
+  const size_t es = (size_t)dtype_size(in->dtype), nn = (size_t)std::max<int64_t>(n, 1);
+  const size_t oes = out->dtype == HB_F32 ? 4 : 8;
+  cudaStream_t s;
+  cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+  PoolAlloc pa{g_dev[device].pool, s};
+  double* d2a = (double*)pa.get(nn * 8);
+  double* d2b = (double*)pa.get(nn * 8);
+  void* work = pa.get(edt_workspace_bytes(in->nz, in->ny, in->nx));
+  const void* d_in = in->data;
+  if (in->location != HB_DEVICE && work) {
+    void* b = pa.get(nn * es);
+    if (b) e = cudaMemcpyAsync(b, in->data, (size_t)n * es, cudaMemcpyHostToDevice, s);
+    d_in = b;
+  }
+  void* d_out = out->location == HB_DEVICE ? out->data : (work ? pa.get(nn * oes) : nullptr);
+  if (!d2a || !d2b || !work || !d_in || !d_out || pa.err != cudaSuccess)
+    e = pa.err != cudaSuccess ? pa.err : cudaErrorMemoryAllocation;
+  if (e == cudaSuccess)
+    e = edt(d_in, in->dtype, in->nz, in->ny, in->nx, spacing, out->dtype != HB_F32, d_out, d2a, d2b,
+            work, s);
+  if (e == cudaSuccess && out->location != HB_DEVICE)
+    e = cudaMemcpyAsync(out->data, d_out, (size_t)n * oes, cudaMemcpyDeviceToHost, s);
+  cudaError_t se = cudaStreamSynchronize(s);
+  if (e == cudaSuccess) e = se;
+  pa.release();
+  cudaStreamSynchronize(s);
+  cudaStreamDestroy(s);
+  if (g_dev[device].session.load() == 0) cudaMemPoolTrimTo(g_dev[device].pool, 0);
+  if (e != cudaSuccess) {
+    set_err(nullptr, std::string("edt: ") + cudaGetErrorString(e));
+    cudaGetLastError();
+    return e == cudaErrorMemoryAllocation ? HB_EBUDGET_UNAVAILABLE : HB_ECUDA;
+  }
+  return HB_OK;
+}
+
 int32_t hb_histogram(const hb_volume* in, int32_t device, int32_t bins, double lo, double hi,
                      const double* edges, int32_t edges_f32, int64_t* counts) {
   if (!in || bins < 1 || !edges || !counts || !(hi > lo) || !std::isfinite(lo) || !std::isfinite(hi)) {

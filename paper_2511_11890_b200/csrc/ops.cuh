@@ -112,6 +112,10 @@ cudaError_t connected_components(const void* in, int dt, int64_t nz, int64_t ny,
                                  int conn, uint32_t* out, int* lab, int* flag, int* ids,
                                  void* scan_tmp, size_t scan_bytes, int64_t* count, cudaStream_t s);
 size_t connected_components_scan_bytes(int64_t n);
+// exact EDT (edt.cu): d2a/d2b: n doubles each; work: edt_workspace_bytes
+size_t edt_workspace_bytes(int64_t nz, int64_t ny, int64_t nx);
+cudaError_t edt(const void* in, int dt, int64_t nz, int64_t ny, int64_t nx, const double* spacing,
+                bool squared, void* out, double* d2a, double* d2b, void* work, cudaStream_t s);
 // geodesic reconstruction (extra.cu); cudaErrorInvalidValue = marker ordering violated
 cudaError_t geodesic(const void* marker, const void* mask, int dt, int64_t nz, int64_t ny, int64_t nx,
                      bool dilation, void* out, int* flags, cudaStream_t s, int64_t* sweeps);

@@ -284,6 +284,18 @@ def _run_geodesic(data, params, budget, cancel):
     return out, ExecutionReport(chunk_count=1)
 
 
+def _run_edt(data, params, budget, cancel):
+    from . import quantify
+    from .ledger import LEDGER
+
+    LEDGER.job_start()
+    out = quantify.edt(data, params.get("spacing") or (1.0, 1.0, 1.0))
+    return out, ExecutionReport(chunk_count=1)
+
+
+register(Operator(name="edt", kind="global", output="volume",
+                  schema={"spacing": (lambda v: tuple(float(s) for s in v), None)},
+                  run=_run_edt, label_input=True))
 register(Operator(name="geodesic_reconstruct", kind="global", output="volume",
                   schema={"marker": (np.asarray, REQUIRED), "kind": (str, "dilation")},
                   run=_run_geodesic, label_input=True))

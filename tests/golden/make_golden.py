@@ -109,6 +109,11 @@ def main():
                 add(f"remove_islands_{vol}_{conn}_{ms}", "remove_islands",
                     {"min_size": ms, "connectivity": conn}, vol,
                     ref.morphology.remove_islands(src, ms, conn))
+    # exact EDT (registry.py:404-417)
+    for vol in ("bin_a", "holes_a", "lab_a"):
+        for sp in ((1.0, 1.0, 1.0), (2.0, 0.5, 0.75)):
+            add(f"edt_{vol}_{sp[0]}", "edt", {"spacing": list(sp)}, vol,
+                Q.edt(arrays[f"in__{vol}"], sp))
     # geodesic reconstruction (registry.py:386-401): marker in params (array key)
     for vol, kind in (("u8_a", "dilation"), ("u16_a", "erosion"), ("f32_unit", "dilation")):
         src = arrays[f"in__{vol}"]

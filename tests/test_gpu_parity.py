@@ -477,3 +477,17 @@ def test_geodesic_reconstruct_vs_oracle(hb, oracle):
                               oracle.geodesic_reconstruct(m_ero, mask, "erosion"))
     with pytest.raises(ParameterError):
         morphology.geodesic_reconstruct(mask.max() + np.zeros_like(mask) + 1, mask, "dilation")
+
+
+def test_edt_vs_oracle(hb, oracle):
+    """quantify.py:115-175: bit-exact float32 distances and float64 squared
+    distances, anisotropic spacing, no-background volumes (+inf)."""
+    from paper_2511_11890_b200 import quantify
+
+    rng = np.random.default_rng(41)
+    for shape in ((24, 33, 40), (1, 7, 64), (50, 1, 1), (16, 16, 16)):
+        for dens in (0.7, 0.98, 1.0):
+            m = (rng.random(shape) < dens).astype(np.uint8)
+            for sp in ((1.0, 1.0, 1.0), (2.0, 0.5, 0.75)):
+                assert np.array_equal(quantify.edt(m, sp), oracle.edt(m, sp)), (shape, dens, sp)
+                assert np.array_equal(quantify.edt(m, sp, squared=True), oracle.edt(m, sp, squared=True))

@@ -82,7 +82,8 @@ class TestRegistry:
             # SURVEY.md §8(f) row 2
             "hessian_xx", "hessian_yy", "hessian_zz", "hessian_xy", "hessian_xz", "hessian_yz",
             "sobel", "prewitt", "apply_threshold", "lbp2d", "anisotropic_diffusion", "otsu",
-            "connected_components", "fill_holes", "remove_islands", "geodesic_reconstruct"}
+            "connected_components", "fill_holes", "remove_islands", "geodesic_reconstruct",
+            "edt"}
 
     def test_profiles_match_reference(self, golden):
         meta, _ = golden
