@@ -49,7 +49,10 @@ typedef enum {
 } hb_status;
 
 /* volume.py:17-23 SUPPORTED_DTYPES + LABEL_DTYPE */
-typedef enum { HB_U8 = 0, HB_U16 = 1, HB_U32 = 2, HB_F32 = 3 } hb_dtype;
+typedef enum {
+  HB_U8 = 0, HB_U16 = 1, HB_U32 = 2, HB_F32 = 3,
+  HB_F64 = 4 /* output only: hb_edt's squared distances */
+} hb_dtype;
 
 typedef enum { HB_HOST = 0, HB_DEVICE = 1 } hb_location;
 
@@ -223,7 +226,7 @@ int32_t hb_geodesic(const hb_volume* marker, const hb_volume* mask, hb_volume* o
 /* Exact Euclidean distance transform (quantify.py:115-175): distance of every
  * nonzero voxel to the nearest zero voxel with per-axis `spacing` (z, y, x).
  * out dtype HB_F32: sqrt(d^2) cast to float32 (the reference's default);
- * out dtype 4 (float64, squared=True): d^2.  No zero voxel -> +inf. */
+ * out dtype HB_F64 (squared=True): d^2.  No zero voxel -> +inf. */
 int32_t hb_edt(const hb_volume* in, hb_volume* out, const double* spacing, int32_t device);
 
 /* Pinned-host helpers (cudaHostRegister for the duration of a job). */

@@ -988,8 +988,7 @@ int32_t hb_geodesic(const hb_volume* marker, const hb_volume* mask, hb_volume* o
 }
 
 int32_t hb_edt(const hb_volume* in, hb_volume* out, const double* spacing, int32_t device) {
-  const int kF64 = 4;
-  if (!in || !out || !in->data || !out->data || !spacing || (out->dtype != HB_F32 && out->dtype != kF64) ||
+  if (!in || !out || !in->data || !out->data || !spacing || (out->dtype != HB_F32 && out->dtype != HB_F64) ||
       in->nz != out->nz || in->ny != out->ny || in->nx != out->nx || in->dtype < HB_U8 || in->dtype > HB_F32) {
     set_err(nullptr, "hb_edt: float32 (or float64 squared) output of the input's shape required");
     return HB_EPARAM;

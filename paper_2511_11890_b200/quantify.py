@@ -72,7 +72,7 @@ def edt(mask, spacing=(1.0, 1.0, 1.0), squared: bool = False):
     out = np.empty(x.shape, np.float64 if squared else np.float32)
     vin, _ = _native._volume_of(x)
     vout = _native.HbVolume(out.ctypes.data, 4 if squared else _native.DTYPE_CODE[np.dtype(np.float32)],
-                            _native.HB_HOST, *out.shape)
+                            _native.HB_HOST, *out.shape)  # 4 = HB_F64 (squared output only)
     rc = _native.load().hb_edt(ctypes.byref(vin), ctypes.byref(vout), sp.ctypes.data,
                                _native.current_device())
     _native.raise_for_status(rc, _native.last_error())
