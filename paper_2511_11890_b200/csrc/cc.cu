@@ -224,6 +224,49 @@ cudaError_t connected_components(const void* in, int dt, int64_t nz, int64_t ny,
   return cudaGetLastError();
 }
 
+// chunked labelling, pass 1 / 2 helpers: rank[i] = position of i's root among
+// the chunk's roots (ascending index = scan order), -1 off the mask
+__global__ void __launch_bounds__(kCT)
+k_cc_rank(const int* __restrict__ root, const int* __restrict__ ids, int n, int* __restrict__ rank) {
+  for (int i = blockIdx.x * kCT + threadIdx.x; i < n; i += gridDim.x * kCT) {
+    const int r = root[i];
+    rank[i] = r >= 0 ? ids[r] : -1;
+  }
+}
+
+__global__ void __launch_bounds__(kCT)
+k_cc_table(const int* __restrict__ rank, int n, const uint32_t* __restrict__ table, uint32_t* __restrict__ out) {
+  for (int i = blockIdx.x * kCT + threadIdx.x; i < n; i += gridDim.x * kCT) {
+    const int r = rank[i];
+    out[i] = r >= 0 ? table[r] : 0u;
+  }
+}
+
+cudaError_t cc_chunk_ranks(const void* in, int dt, int cz, int ny, int nx, int conn, int* lab, int* root,
+                           int* flag, int* ids, void* scan_tmp, size_t scan_bytes, int* rank,
+                           int64_t* nroots, cudaStream_t s) {
+  const int n = cz * ny * nx;
+  const int g = cgrid(n);
+  cudaError_t e = cc_label<CC_NONZERO>(in, dt, cz, ny, nx, conn, lab, root, flag, s);
+  if (e != cudaSuccess) return e;
+  size_t need = scan_bytes;
+  e = cub::DeviceScan::ExclusiveSum(scan_tmp, need, flag, ids, n, s);
+  if (e != cudaSuccess) return e;
+  k_cc_rank<<<g, kCT, 0, s>>>(root, ids, n, rank);
+  int last_id = 0, last_flag = 0;
+  cudaMemcpyAsync(&last_id, ids + n - 1, 4, cudaMemcpyDeviceToHost, s);
+  cudaMemcpyAsync(&last_flag, flag + n - 1, 4, cudaMemcpyDeviceToHost, s);
+  e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return e;
+  *nroots = (int64_t)last_id + last_flag;
+  return cudaGetLastError();
+}
+
+cudaError_t cc_apply_table(const int* rank, int n, const uint32_t* table, uint32_t* out, cudaStream_t s) {
+  k_cc_table<<<cgrid(n), kCT, 0, s>>>(rank, n, table, out);
+  return cudaGetLastError();
+}
+
 cudaError_t label_filter(const void* in, int dt, int64_t nz, int64_t ny, int64_t nx, int conn,
                          int op, int64_t min_size, void* out, int* lab, int* root, int* aux,
                          cudaStream_t s) {

@@ -649,6 +649,129 @@ int32_t for_each_slab(const hb_volume* in, int32_t dev, F&& fn) {
 }
 }  // namespace
 
+// ---------------------------------------------------------------------------
+// Chunked connected components (quantify.py:73-111): volumes beyond one
+// device pass are labelled z-chunk by z-chunk.  Pass 1 labels each chunk on
+// the device (roots numbered in scan order -> "candidates", globally ordered
+// by chunk then rank) and unions candidates that touch across each chunk
+// boundary (the reference's boundary union-find, smaller candidate wins);
+// the final ids number the surviving candidates in order, which is the
+// global first-voxel order.  Pass 2 relabels each chunk through the table.
+// ---------------------------------------------------------------------------
+namespace {
+int64_t dsu_find(std::vector<int64_t>& p, int64_t x) {
+  while (p[x] != x) {
+    p[x] = p[p[x]];
+    x = p[x];
+  }
+  return x;
+}
+
+int32_t cc_chunked(const hb_volume* in, hb_volume* out, int conn, int dev, int64_t cs, int64_t* count) {
+  const int64_t nz = in->nz, ny = in->ny, nx = in->nx, plane = ny * nx;
+  const size_t es = (size_t)dtype_size(in->dtype);
+  const int64_t nchunks = (nz + cs - 1) / cs;
+  cudaStream_t s;
+  cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+  PoolAlloc pa{g_dev[dev].pool, s};
+  const size_t cn = (size_t)(cs * plane);
+  const size_t scan_bytes = connected_components_scan_bytes((int64_t)cn) + 256;
+  void* d_in = pa.get(cn * es);
+  int* lab = (int*)pa.get(cn * 4);
+  int* root = (int*)pa.get(cn * 4);
+  int* flag = (int*)pa.get(cn * 4);
+  int* ids = (int*)pa.get(cn * 4);
+  int* rank = (int*)pa.get(cn * 4);
+  void* tmp = pa.get(scan_bytes);
+  uint32_t* table = (uint32_t*)pa.get(cn * 4);
+  uint32_t* d_out = (uint32_t*)pa.get(cn * 4);
+  cudaError_t e = (!d_in || !lab || !root || !flag || !ids || !rank || !tmp || !table || !d_out)
+                      ? (pa.err != cudaSuccess ? pa.err : cudaErrorMemoryAllocation)
+                      : cudaSuccess;
+  std::vector<int64_t> offs(nchunks + 1, 0), parent;
+  std::vector<int> prev_last((size_t)plane), first((size_t)plane), last((size_t)plane);
+  auto load_chunk = [&](int64_t c, int64_t& cz) -> cudaError_t {
+    const int64_t z0 = c * cs;
+    cz = std::min(cs, nz - z0);
+    const size_t bytes = (size_t)(cz * plane) * es;
+    const char* src = (const char*)in->data + (size_t)(z0 * plane) * es;
+    return cudaMemcpyAsync(d_in, src, bytes, in->location == HB_DEVICE ? cudaMemcpyDeviceToDevice
+                                                                           : cudaMemcpyHostToDevice, s);
+  };
+  // pass 1: per-chunk candidates + boundary unions
+  for (int64_t c = 0; c < nchunks && e == cudaSuccess; ++c) {
+    int64_t cz = 0, nr = 0;
+    e = load_chunk(c, cz);
+    if (e == cudaSuccess)
+      e = cc_chunk_ranks(d_in, in->dtype, (int)cz, (int)ny, (int)nx, conn, lab, root, flag, ids, tmp,
+                         scan_bytes, rank, &nr, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(first.data(), rank, (size_t)plane * 4, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(last.data(), rank + (cz - 1) * plane, (size_t)plane * 4, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) break;
+    offs[c + 1] = offs[c] + nr;
+    parent.resize((size_t)offs[c + 1]);
+    for (int64_t k = offs[c]; k < offs[c + 1]; ++k) parent[(size_t)k] = k;
+    if (c > 0) {
+      for (int64_t y = 0; y < ny; ++y)
+        for (int64_t x = 0; x < nx; ++x) {
+          const int b = first[(size_t)(y * nx + x)];
+          if (b < 0) continue;
+          for (int dy = -1; dy <= 1; ++dy)
+            for (int dx = -1; dx <= 1; ++dx) {
+              if (conn == 6 && (dy != 0 || dx != 0)) continue;
+              const int64_t yy = y + dy, xx = x + dx;
+              if (yy < 0 || yy >= ny || xx < 0 || xx >= nx) continue;
+              const int a = prev_last[(size_t)(yy * nx + xx)];
+              if (a < 0) continue;
+              int64_t ra = dsu_find(parent, offs[c - 1] + a), rb = dsu_find(parent, offs[c] + b);
+              if (ra == rb) continue;
+              if (ra < rb) parent[(size_t)rb] = ra;
+              else parent[(size_t)ra] = rb;
+            }
+        }
+    }
+    prev_last.swap(last);
+  }
+  // final ids in candidate order (= first-voxel scan order); roots precede members
+  std::vector<uint32_t> fin(parent.size());
+  int64_t cnt = 0;
+  for (size_t k = 0; e == cudaSuccess && k < parent.size(); ++k) {
+    const int64_t r = dsu_find(parent, (int64_t)k);
+    fin[k] = r == (int64_t)k ? (uint32_t)(++cnt) : fin[(size_t)r];
+  }
+  // pass 2: relabel every chunk through its slice of the table
+  for (int64_t c = 0; c < nchunks && e == cudaSuccess; ++c) {
+    int64_t cz = 0, nr = 0;
+    e = load_chunk(c, cz);
+    if (e == cudaSuccess)
+      e = cc_chunk_ranks(d_in, in->dtype, (int)cz, (int)ny, (int)nx, conn, lab, root, flag, ids, tmp,
+                         scan_bytes, rank, &nr, s);
+    if (e == cudaSuccess && nr > 0)
+      e = cudaMemcpyAsync(table, fin.data() + offs[c], (size_t)nr * 4, cudaMemcpyHostToDevice, s);
+    uint32_t* dst = out->location == HB_DEVICE ? (uint32_t*)out->data + c * cs * plane : d_out;
+    if (e == cudaSuccess) e = cc_apply_table(rank, (int)(cz * plane), table, dst, s);
+    if (e == cudaSuccess && out->location != HB_DEVICE)
+      e = cudaMemcpyAsync((uint32_t*)out->data + c * cs * plane, d_out, (size_t)(cz * plane) * 4,
+                          cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // the host table slice / d_out are reused
+  }
+  cudaStreamSynchronize(s);
+  pa.release();
+  cudaStreamSynchronize(s);
+  cudaStreamDestroy(s);
+  if (g_dev[dev].session.load() == 0) cudaMemPoolTrimTo(g_dev[dev].pool, 0);
+  if (e != cudaSuccess) {
+    set_err(nullptr, std::string("connected components (chunked): ") + cudaGetErrorString(e));
+    cudaGetLastError();
+    return e == cudaErrorMemoryAllocation ? HB_EBUDGET_UNAVAILABLE : HB_ECUDA;
+  }
+  if (count) *count = cnt;
+  return HB_OK;
+}
+}  // namespace
+
 extern "C" {
 
 int32_t hb_abi_version(void) { return HB_ABI_VERSION; }
@@ -803,16 +926,36 @@ int32_t hb_connected_components(const hb_volume* in, hb_volume* out, int32_t con
     return HB_EBUDGET_UNAVAILABLE;
   }
   const int64_t n = in->nz * in->ny * in->nx;
-  if (n >= (1ll << 31) - 1) {
-    set_err(nullptr, "connected components: volumes of 2^31 voxels or more are not supported");
-    return HB_EUNSUPPORTED;
-  }
   std::lock_guard<std::mutex> lk(g_dev[device].mu);
   cudaSetDevice(device);
   cudaError_t e = ensure_pool(device);
   if (e != cudaSuccess) {
     set_err(nullptr, cudaGetErrorString(e));
     return HB_ECUDA;
+  }
+  {
+    // one device pass when the volume fits (int32 indices, ~22 B/voxel of
+    // scratch); otherwise z-chunks with the boundary union-find.
+    // HB_CC_CHUNK_SLICES forces a chunk height (tests).
+    const int64_t plane = std::max<int64_t>(1, in->ny * in->nx);
+    const size_t es = (size_t)dtype_size(in->dtype);
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    const double per_voxel = 22.0 + (double)es;
+    int64_t cs = 0;
+    if (const char* env = std::getenv("HB_CC_CHUNK_SLICES")) cs = std::atoll(env);
+    if (cs <= 0 && (n >= (1ll << 31) - 1 || (double)n * per_voxel > 0.8 * (double)fr)) {
+      const int64_t by_index = ((1ll << 31) - 2) / plane;
+      const int64_t by_mem = (int64_t)(0.6 * (double)fr / (per_voxel * (double)plane));
+      cs = std::max<int64_t>(1, std::min(by_index, by_mem));
+    }
+    if (cs > 0 && cs < in->nz) {
+      if (cs * plane >= (1ll << 31) - 1) {
+        set_err(nullptr, "connected components: one slice exceeds 2^31 voxels");
+        return HB_EUNSUPPORTED;
+      }
+      return cc_chunked(in, out, connectivity, device, cs, count);
+    }
   }
   cudaStream_t s;
   cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);

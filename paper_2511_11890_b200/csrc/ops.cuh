@@ -112,6 +112,12 @@ cudaError_t connected_components(const void* in, int dt, int64_t nz, int64_t ny,
                                  int conn, uint32_t* out, int* lab, int* flag, int* ids,
                                  void* scan_tmp, size_t scan_bytes, int64_t* count, cudaStream_t s);
 size_t connected_components_scan_bytes(int64_t n);
+// chunked labelling (volumes beyond one device pass): per chunk, the rank of
+// every voxel's root among the chunk's roots, and the final table lookup
+cudaError_t cc_chunk_ranks(const void* in, int dt, int cz, int ny, int nx, int conn, int* lab, int* root,
+                           int* flag, int* ids, void* scan_tmp, size_t scan_bytes, int* rank,
+                           int64_t* nroots, cudaStream_t s);
+cudaError_t cc_apply_table(const int* rank, int n, const uint32_t* table, uint32_t* out, cudaStream_t s);
 // exact EDT (edt.cu): d2a/d2b: n doubles each; work: edt_workspace_bytes
 size_t edt_workspace_bytes(int64_t nz, int64_t ny, int64_t nx);
 cudaError_t edt(const void* in, int dt, int64_t nz, int64_t ny, int64_t nx, const double* spacing,
