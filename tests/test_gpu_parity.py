@@ -509,3 +509,32 @@ def test_connected_components_chunked_vs_oracle(hb, oracle, slices, monkeypatch)
                 want, n = oracle.connected_components(m, conn)
                 got, k = quantify.connected_components(m, conn)
                 assert k == n and np.array_equal(got, want), (shape, dens, conn)
+
+
+@pytest.mark.parametrize("steps", [
+    [("gaussian", {"sigma": 1.0, "precision": "exact"}), ("apply_threshold", {"t": 0.5})],
+    [("sobel", {}), ("median", {"radius": 1})],
+    [("anisotropic_diffusion", {"iterations": 2, "kappa": 0.4, "mode": "rational"}), ("lbp2d", {})],
+    [("hessian_xy", {"sigma": 1.0}), ("morph_dilate", {"se": "box:1"})],
+])
+def test_pipelines_of_next_ops(hb, oracle, steps):
+    """run_pipeline fuses the §8(f) ops with the hot-path ones into one device
+    chain per chunk: chunked (3+ chunks) == the oracle applied op by op."""
+    from conftest import budget_for
+    from paper_2511_11890_b200 import registry
+    from paper_2511_11890_b200.chunking import OpProfile
+
+    x = np.random.default_rng(5).random((40, 33, 28), dtype=np.float32)
+    want = x
+    halo = 0
+    for name, p in steps:
+        q = dict(p)
+        q.pop("precision", None)
+        if name.startswith("morph_"):
+            want = oracle.morph(want, name[6:], oracle.parse_se(q["se"]), 1)
+        else:
+            want = oracle.apply(name, want, q)
+        halo += registry.get_operator(name).profile(registry.validate_params(registry.get_operator(name), p)).halo_z
+    got, rep = registry.run_pipeline(x, steps, budget_for(OpProfile(halo, 12), x.shape, x.dtype, 6))
+    assert rep.chunk_count >= 3
+    assert got.dtype == want.dtype and np.array_equal(got, want)
