@@ -9,6 +9,7 @@
 // once per slice (x direction), and folds the rows (y, z directions) for each
 // output — for ball:3 that is 29 row terms instead of 123 offsets.
 #include <vector>
+#include <cstdlib>
 #include <algorithm>
 #include <array>
 #include <map>
@@ -542,10 +543,29 @@ __device__ __forceinline__ uint32_t op3x2(uint32_t a, uint32_t b, uint32_t c) {
   return op2x2<MAX>(op2x2<MAX>(a, b), c);  // ptxas fuses into VIMNMX3.U16x2
 }
 
-template <typename T, bool MAX, int KIND, int R>
+// BIN (uint8 only): a {0,1} volume, where min/max are AND/OR of whole words —
+// four voxels per 32-bit op (LOP3 folds three), no u16 widening.  `gate`
+// (device): 0 = the block is binary, 1 = grey; the BIN and grey u8 kernels
+// are both enqueued and each returns at once unless the gate selects it.
+template <bool MAX, bool BIN>
+__device__ __forceinline__ uint32_t mop2(uint32_t a, uint32_t b) {
+  if constexpr (BIN) return MAX ? (a | b) : (a & b);
+  else return op2x2<MAX>(a, b);
+}
+template <bool MAX, bool BIN>
+__device__ __forceinline__ uint32_t mop3(uint32_t a, uint32_t b, uint32_t c) {
+  if constexpr (BIN) return MAX ? (a | b | c) : (a & b & c);
+  else return op3x2<MAX>(a, b, c);
+}
+
+template <typename T, bool MAX, int KIND, int R, bool BIN>
 __global__ void __launch_bounds__(M3X_NT, 2)
-k_morph3(const __grid_constant__ CUtensorMap tin, T* __restrict__ out, const Morph3Args a) {
+k_morph3(const __grid_constant__ CUtensorMap tin, T* __restrict__ out, const Morph3Args a,
+         const int* __restrict__ gate) {
+  static_assert(!BIN || sizeof(T) == 1, "the binary path is uint8 only");
+  if (gate != nullptr && ((*gate != 0) == BIN)) return;  // the other variant runs
   using S = SeShape<KIND, R>;
+  constexpr int NW = BIN ? 1 : 2;  // 32-bit words per thread (4 voxels)
   constexpr int ALIGN = 16 / (int)sizeof(T);
   constexpr int XA = (R + ALIGN - 1) / ALIGN * ALIGN < 4 ? 4 : (R + ALIGN - 1) / ALIGN * ALIGN;
   constexpr int XA2 = (XA + ALIGN - 1) / ALIGN * ALIGN;   // box start offset (>= 4, 16-B aligned)
@@ -554,7 +574,7 @@ k_morph3(const __grid_constant__ CUtensorMap tin, T* __restrict__ out, const Mor
   constexpr int STAGE_BYTES = HY * WBOX * (int)sizeof(T);
   constexpr int STAGE_PITCH = (STAGE_BYTES + 127) / 128 * 128;
   constexpr int RING = 2 * R + 1;
-  constexpr int WPR = M3X_TX / 2;  // u16x2 words per H row (32)
+  constexpr int WPR = BIN ? M3X_TX / 4 : M3X_TX / 2;  // words per H row
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem =
       smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u)  /* stays in .shared */;
@@ -583,10 +603,12 @@ k_morph3(const __grid_constant__ CUtensorMap tin, T* __restrict__ out, const Mor
 
   // V/Z ownership: row vy, 4-wide x block vq (two u16x2 words: pairs 2vq, 2vq+1)
   const int vq = tid % M3X_Q, vy = tid / M3X_Q;  // vy in [0, 32)
-  uint32_t acc[RING][2];
+  uint32_t acc[RING][NW];
   constexpr uint32_t IDENT = MAX ? 0u : 0xffffffffu;
 #pragma unroll
-  for (int u = 0; u < RING; ++u) acc[u][0] = acc[u][1] = IDENT;
+  for (int u = 0; u < RING; ++u)
+#pragma unroll
+    for (int j = 0; j < NW; ++j) acc[u][j] = IDENT;
 
   // load the u16x2 word covering x = (tile) 2p, 2p+1 of stage row r
   auto word = [&](const T* row, int p) -> uint32_t {
@@ -606,12 +628,18 @@ k_morph3(const __grid_constant__ CUtensorMap tin, T* __restrict__ out, const Mor
   const int64_t oplane = (int64_t)a.ny * a.nx;
   auto store_out = [&](int o, uint32_t v0, uint32_t v1) {
     T* dst = obase + o * oplane;
-    if (st_full) {
-      if constexpr (sizeof(T) == 2) *reinterpret_cast<uint2*>(dst) = make_uint2(v0, v1);
-      else *reinterpret_cast<uint32_t*>(dst) = prmt(v0, v1, 0x6420);
-    } else if (st_part) {
-      const uint32_t vv[2] = {v0, v1};
-      for (int i = 0; i < 4 && gx + i < a.nx; ++i) dst[i] = (T)((vv[i >> 1] >> (16 * (i & 1))) & 0xffffu);
+    if constexpr (BIN) {
+      if (st_full) *reinterpret_cast<uint32_t*>(dst) = v0;
+      else if (st_part)
+        for (int i = 0; i < 4 && gx + i < a.nx; ++i) dst[i] = (T)((v0 >> (8 * i)) & 0xffu);
+    } else {
+      if (st_full) {
+        if constexpr (sizeof(T) == 2) *reinterpret_cast<uint2*>(dst) = make_uint2(v0, v1);
+        else *reinterpret_cast<uint32_t*>(dst) = prmt(v0, v1, 0x6420);
+      } else if (st_part) {
+        const uint32_t vv[2] = {v0, v1};
+        for (int i = 0; i < 4 && gx + i < a.nx; ++i) dst[i] = (T)((vv[i >> 1] >> (16 * (i & 1))) & 0xffffu);
+      }
     }
   };
 
@@ -633,6 +661,28 @@ k_morph3(const __grid_constant__ CUtensorMap tin, T* __restrict__ out, const Mor
         if (item >= HY * M3X_Q) break;
         const int r = item / M3X_Q, q = item % M3X_Q;
         const T* row = stage + r * WBOX;
+        if constexpr (BIN) {
+          // words of 4 voxels: w[0] = voxels 4q-4..4q-1, w[1] = 4q..4q+3, w[2] = 4q+4..4q+7;
+          // shift(d) picks bytes across word boundaries with one PRMT
+          uint32_t wb[3];
+#pragma unroll
+          for (int i = 0; i < 3; ++i) wb[i] = *reinterpret_cast<const uint32_t*>(row + XA2 + 4 * q - 4 + 4 * i);
+          auto shb = [&](int d) -> uint32_t {
+            if (d == 0) return wb[1];
+            // bytes (4 + d) .. (7 + d) of the 12-byte window wb[0..2]
+            const int b0 = 4 + d;
+            const uint32_t lo = b0 < 4 ? wb[0] : wb[1], hi = b0 < 4 ? wb[1] : wb[2];
+            const int o = b0 & 3;
+            const uint32_t sel = (uint32_t)(o | ((o + 1) << 4) | ((o + 2) << 8) | ((o + 3) << 12));
+            return prmt(lo, hi, sel);
+          };
+          uint32_t h = wb[1];
+#pragma unroll
+          for (int k = 1; k <= R; ++k) {
+            h = mop3<MAX, BIN>(h, shb(-k), shb(k));
+            if (S::needs(k)) sH[((k - 1) * HY + r) * WPR + q] = h;
+          }
+        } else {
         uint32_t w[6];  // pairs 2q-2 .. 2q+3
 #pragma unroll
         for (int i = 0; i < 6; ++i) {
@@ -663,19 +713,22 @@ k_morph3(const __grid_constant__ CUtensorMap tin, T* __restrict__ out, const Mor
             if (S::needs(k)) sH[((k - 1) * HY + r) * WPR + 2 * q + j] = h;
           }
         }
+        }  // !BIN
       }
     }
     __syncthreads();
     // ---- V: every layer's 2D shape for this thread's 4 outputs ----------------
     // rows of one layer are folded three at a time (VIMNMX3.U16x2); the two
     // words of a row come from one LDS.64; identical loads across layers CSE
-    uint32_t layer[R + 1][2];
+    uint32_t layer[R + 1][NW];
     {
-      const uint32_t* hb = sH + (vy + R) * WPR + 2 * vq;  // H_k row r: hb[((k-1)*HY + r-vy-R)*WPR]
+      const uint32_t* hb = sH + (vy + R) * WPR + NW * vq;  // H_k row r: hb[((k-1)*HY + r-vy-R)*WPR]
       const T* rb = stage + (vy + R) * WBOX + XA2 + 4 * vq;
       auto term = [&](int k, int dy, int j) -> uint32_t {
         if (k == 0) {
-          if constexpr (sizeof(T) == 2) {
+          if constexpr (BIN) {
+            return *reinterpret_cast<const uint32_t*>(rb + dy * WBOX);
+          } else if constexpr (sizeof(T) == 2) {
             return *reinterpret_cast<const uint32_t*>(rb + dy * WBOX + 2 * j);
           } else {
             const uint32_t b4 = *reinterpret_cast<const uint32_t*>(rb + dy * WBOX);
@@ -687,7 +740,7 @@ k_morph3(const __grid_constant__ CUtensorMap tin, T* __restrict__ out, const Mor
 #pragma unroll
       for (int L = 0; L <= R; ++L) {
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
+        for (int j = 0; j < NW; ++j) {
           uint32_t v = 0;
           int nt = 0;
           uint32_t pend = 0;
@@ -703,12 +756,12 @@ k_morph3(const __grid_constant__ CUtensorMap tin, T* __restrict__ out, const Mor
               pend = t;
               has_pend = true;
             } else {
-              v = op3x2<MAX>(v, pend, t);
+              v = mop3<MAX, BIN>(v, pend, t);
               has_pend = false;
             }
             ++nt;
           }
-          if (has_pend) v = op2x2<MAX>(v, pend);
+          if (has_pend) v = mop2<MAX, BIN>(v, pend);
           layer[L][j] = v;
         }
       }
@@ -723,13 +776,13 @@ k_morph3(const __grid_constant__ CUtensorMap tin, T* __restrict__ out, const Mor
         const int slot = ((U - d - R) % RING + RING) % RING; /* o = s - d - R */        \
         const int L = d < 0 ? -d : d;                                                   \
         if (d == R) {                                                                   \
-          const uint32_t v0 = op2x2<MAX>(acc[slot][0], layer[L][0]);                    \
-          const uint32_t v1 = op2x2<MAX>(acc[slot][1], layer[L][1]);                    \
+          const uint32_t v0 = mop2<MAX, BIN>(acc[slot][0], layer[L][0]);                \
+          const uint32_t v1 = NW > 1 ? mop2<MAX, BIN>(acc[slot][NW - 1], layer[L][NW - 1]) : 0u; \
           if (s >= 2 * R) store_out(s - 2 * R, v0, v1);                                 \
-          acc[slot][0] = acc[slot][1] = IDENT;                                          \
+          _Pragma("unroll") for (int j = 0; j < NW; ++j) acc[slot][j] = IDENT;          \
         } else {                                                                        \
-          acc[slot][0] = op2x2<MAX>(acc[slot][0], layer[L][0]);                         \
-          acc[slot][1] = op2x2<MAX>(acc[slot][1], layer[L][1]);                         \
+          _Pragma("unroll") for (int j = 0; j < NW; ++j)                                \
+            acc[slot][j] = mop2<MAX, BIN>(acc[slot][j], layer[L][j]);                   \
         }                                                                               \
       }                                                                                 \
     }                                                                                   \
@@ -778,15 +831,16 @@ bool classify_se(const int32_t* off, int n, int& kind, int& r) {
   return false;
 }
 
-template <typename T, bool MAX, int KIND, int R>
-cudaError_t launch_morph3(const DevIn& in, int64_t zo, int64_t nzo, void* out, cudaStream_t s) {
+template <typename T, bool MAX, int KIND, int R, bool BIN>
+cudaError_t launch_morph3_v(const DevIn& in, int64_t zo, int64_t nzo, void* out, const int* gate,
+                            cudaStream_t s) {
   constexpr int ALIGN = 16 / (int)sizeof(T);
   constexpr int XA = (R + ALIGN - 1) / ALIGN * ALIGN < 4 ? 4 : (R + ALIGN - 1) / ALIGN * ALIGN;
   constexpr int XA2 = (XA + ALIGN - 1) / ALIGN * ALIGN;
   constexpr int WBOX = (XA2 + M3X_TX + XA2 + ALIGN - 1) / ALIGN * ALIGN;
   constexpr int HY = M3X_TY + 2 * R;
   constexpr int STAGE_PITCH = (HY * WBOX * (int)sizeof(T) + 127) / 128 * 128;
-  const int smem = M3X_NST * STAGE_PITCH + R * HY * (M3X_TX / 2) * 4 + M3X_NST * 8 + 128;
+  const int smem = M3X_NST * STAGE_PITCH + R * HY * (M3X_TX / 2) * 4 + M3X_NST * 8 + 128;  // BIN uses half the sH
   CUtensorMap tin;
   const CUtensorMapDataType dt = sizeof(T) == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_UINT16;
   if (!make_tmap_3d(&tin, in.p, dt, sizeof(T), in.nx, in.ny, in.nz, WBOX, HY)) return cudaErrorNotSupported;
@@ -801,10 +855,44 @@ cudaError_t launch_morph3(const DevIn& in, int64_t zo, int64_t nzo, void* out, c
   const int64_t want = std::max<int64_t>(1, (4 * kNumSMs + tiles - 1) / tiles);
   a.zchunk = (int)std::max<int64_t>(std::min<int64_t>(nzo, 8 * R + 8), (nzo + want - 1) / want);
   dim3 grid(gx, gy, (unsigned)((nzo + a.zchunk - 1) / a.zchunk));
-  auto kern = k_morph3<T, MAX, KIND, R>;
+  auto kern = k_morph3<T, MAX, KIND, R, BIN>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  kern<<<grid, M3X_NT, smem, s>>>(tin, (T*)out, a);
+  kern<<<grid, M3X_NT, smem, s>>>(tin, (T*)out, a, gate);
   return cudaGetLastError();
+}
+
+__global__ void k_u8_grey_check(const uint8_t* __restrict__ p, int64_t n, int* __restrict__ grey) {
+  const int64_t n16 = n / 16;
+  bool any = false;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n16; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(p) + i);
+    any |= ((v.x | v.y | v.z | v.w) & 0xfefefefeu) != 0u;
+  }
+  for (int64_t i = n16 * 16 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    any |= p[i] > 1;
+  if (__syncthreads_or(any) && threadIdx.x == 0) *grey = 1;
+}
+
+// u16: the grey kernel.  u8: a device check of the block (any byte > 1?)
+// gates the binary (AND/OR, 4 voxels per op) and the grey kernel; both are
+// enqueued and the unselected one exits at once — no host round trip.
+template <typename T, bool MAX, int KIND, int R>
+cudaError_t launch_morph3(const DevIn& in, int64_t zo, int64_t nzo, void* out, cudaStream_t s) {
+  if constexpr (sizeof(T) == 2) {
+    return launch_morph3_v<T, MAX, KIND, R, false>(in, zo, nzo, out, nullptr, s);
+  } else {
+    if ((reinterpret_cast<uintptr_t>(in.p) & 15) != 0 || std::getenv("HB_MORPH_NOBIN"))
+      return launch_morph3_v<T, MAX, KIND, R, false>(in, zo, nzo, out, nullptr, s);
+    int* gate = nullptr;
+    cudaError_t e = cudaMallocAsync(&gate, sizeof(int), s);
+    if (e != cudaSuccess) return e;
+    cudaMemsetAsync(gate, 0, sizeof(int), s);
+    k_u8_grey_check<<<kNumSMs * 4, 256, 0, s>>>((const uint8_t*)in.p, in.nz * in.ny * in.nx, gate);
+    e = launch_morph3_v<T, MAX, KIND, R, true>(in, zo, nzo, out, gate, s);
+    if (e == cudaSuccess) e = launch_morph3_v<T, MAX, KIND, R, false>(in, zo, nzo, out, gate, s);
+    cudaFreeAsync(gate, s);
+    return e;
+  }
 }
 
 template <typename T, bool MAX>
