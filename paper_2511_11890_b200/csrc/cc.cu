@@ -151,10 +151,16 @@ k_fill(const T* __restrict__ in, const int* __restrict__ root, const int* __rest
   }
 }
 
+// component sizes by root; neighbouring voxels mostly share a root, so the
+// lanes of a warp with equal roots add once (__match_any_sync) instead of
+// serialising on one address (a giant component made this 2.3 Gvox/s)
 __global__ void __launch_bounds__(kCT) k_sizes(const int* __restrict__ root, int n, int* __restrict__ size) {
-  for (int i = blockIdx.x * kCT + threadIdx.x; i < n; i += gridDim.x * kCT) {
-    const int r = root[i];
-    if (r >= 0) atomicAdd(&size[r], 1);
+  for (int i0 = blockIdx.x * kCT; i0 < n; i0 += gridDim.x * kCT) {
+    const int i = i0 + threadIdx.x;
+    const int r = i < n ? root[i] : -1;
+    const unsigned peers = __match_any_sync(0xffffffffu, r);
+    const int leader = __ffs(peers) - 1;
+    if (r >= 0 && (int)(threadIdx.x & 31) == leader) atomicAdd(&size[r], __popc(peers));
   }
 }
 

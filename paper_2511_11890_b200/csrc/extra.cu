@@ -32,12 +32,13 @@ inline int grid_for(int64_t n) {
 __global__ void __launch_bounds__(kT)
 k_hessian_comp(const float* __restrict__ g, int64_t gz0, int nz, int ny, int nx, int64_t zo,
                int64_t nzo, int axis_a, int axis_b, float* __restrict__ out) {
-  const int64_t plane = (int64_t)ny * nx, total = nzo * plane;
   const int n[3] = {nz, ny, nx};
-  for (int64_t i = blockIdx.x * (int64_t)kT + threadIdx.x; i < total; i += (int64_t)gridDim.x * kT) {
-    const int64_t zl = i / plane;
-    const int64_t rr = i - zl * plane;
-    int p[3] = {(int)(zo + zl), (int)(rr / nx), (int)(rr % nx)};
+  // one output row (z, y) per block iteration: no per-voxel 64-bit division
+  for (int64_t row = blockIdx.x; row < nzo * ny; row += gridDim.x)
+  for (int x = threadIdx.x; x < nx; x += kT) {
+    const int64_t i = row * nx + x;
+    const int zl = (int)(row / ny);
+    int p[3] = {(int)(zo + zl), (int)(row - (int64_t)zl * ny), x};
     auto at = [&](const int (&q)[3]) {
       return __ldg(g + ((int64_t)(q[0] - gz0) * ny + q[1]) * nx + q[2]);
     };
@@ -73,11 +74,11 @@ template <typename T>
 __global__ void __launch_bounds__(kT)
 k_gradmag(const T* __restrict__ in, int nz, int ny, int nx, int64_t zo, int64_t nzo,
           float smooth_mid, float* __restrict__ out) {
-  const int64_t plane = (int64_t)ny * nx, total = nzo * plane;
-  for (int64_t i = blockIdx.x * (int64_t)kT + threadIdx.x; i < total; i += (int64_t)gridDim.x * kT) {
-    const int64_t zl = i / plane;
-    const int64_t rr = i - zl * plane;
-    const int z = (int)(zo + zl), y = (int)(rr / nx), x = (int)(rr % nx);
+  for (int64_t row = blockIdx.x; row < nzo * ny; row += gridDim.x)
+  for (int x = threadIdx.x; x < nx; x += kT) {
+    const int64_t i = row * nx + x;
+    const int zl = (int)(row / ny);
+    const int z = (int)(zo + zl), y = (int)(row - (int64_t)zl * ny);
     // the clamped 3x3x3 window (each separable pass clamps along its own axis,
     // which is the same as clamping the window once)
     float v[3][3][3];
@@ -133,11 +134,13 @@ template <typename T>
 __global__ void __launch_bounds__(kT)
 k_lbp2d(const T* __restrict__ in, int ny, int nx, int64_t n, uint8_t* __restrict__ out) {
   const int64_t plane = (int64_t)ny * nx;
-  for (int64_t i = blockIdx.x * (int64_t)kT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kT) {
-    const int64_t zl = i / plane;
-    const int64_t rr = i - zl * plane;
-    const int y = (int)(rr / nx), x = (int)(rr % nx);
+  for (int64_t row = blockIdx.x; row < n / nx; row += gridDim.x)
+  for (int x = threadIdx.x; x < nx; x += kT) {
+    const int64_t i = row * nx + x;
+    const int64_t zl = row / ny;
+    const int y = (int)(row - zl * ny);
     const T* sl = in + zl * plane;
+    const int64_t rr = (int64_t)y * nx + x;
     const T c = __ldg(sl + rr);
     const int ym = max(y - 1, 0) * nx, y0 = y * nx, yp = min(y + 1, ny - 1) * nx;
     const int xm = max(x - 1, 0), xp = min(x + 1, nx - 1);
@@ -168,11 +171,11 @@ __device__ __forceinline__ float diff_g(float v, float kappa, bool rational) {
 __global__ void __launch_bounds__(kT)
 k_diffusion_step(const float* __restrict__ src, float* __restrict__ dst, int nz, int ny, int nx,
                  float kappa, float dt, bool rational) {
-  const int64_t plane = (int64_t)ny * nx, n = (int64_t)nz * plane;
-  for (int64_t i = blockIdx.x * (int64_t)kT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kT) {
-    const int z = (int)(i / plane);
-    const int64_t rr = i - (int64_t)z * plane;
-    const int y = (int)(rr / nx), x = (int)(rr % nx);
+  const int64_t plane = (int64_t)ny * nx;
+  for (int64_t row = blockIdx.x; row < (int64_t)nz * ny; row += gridDim.x)
+  for (int x = threadIdx.x; x < nx; x += kT) {
+    const int64_t i = row * nx + x;
+    const int z = (int)(row / ny), y = (int)(row - (int64_t)z * ny);
     const float c = src[i];
     const int crd[3] = {z, y, x}, ext[3] = {nz, ny, nx};
     const int64_t str[3] = {plane, nx, 1};
