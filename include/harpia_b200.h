@@ -82,10 +82,26 @@ typedef enum {
   HB_OP_PREWITT = 10, /* filters.py:205-207 */
   HB_OP_THRESHOLD = 11, /* threshold.py:110-112; amount = t; uint32 labels */
   HB_OP_LBP2D = 12,   /* filters.py:213-227; uint8 per-slice codes */
-  HB_OP_DIFFUSION = 13 /* anisotropic_diffusion, filters.py:142-184: radius =
+  HB_OP_DIFFUSION = 13, /* anisotropic_diffusion, filters.py:142-184: radius =
                           iterations, sigma = kappa, amount = dt, precision =
                           mode (0 exponential, 1 rational) */
+  HB_OP_LOCAL_THRESHOLD = 14 /* threshold.local_threshold, threshold.py:174-217
+                          (registry.py:257-272): radius = window, precision =
+                          hb_local_kind, sigma = k, amount = c (mean / median /
+                          gaussian) or R (sauvola; NaN = half the
+                          input dtype's range, 0.5 for float32); gaussian: weights64 = the
+                          2*window+1 float64 taps (threshold.py:199-202), NULL =
+                          computed by the library; uint32 labels */
 } hb_op;
+
+/* local_threshold kinds, in threshold.LOCAL_KINDS order (threshold.py:21) */
+typedef enum {
+  HB_LT_MEAN = 0,
+  HB_LT_MEDIAN = 1,
+  HB_LT_GAUSSIAN = 2,
+  HB_LT_NIBLACK = 3,
+  HB_LT_SAUVOLA = 4
+} hb_local_kind;
 
 typedef enum {
   HB_PREC_FAST = 0,  /* fp32 accumulation, within 1e-5 of the reference */
@@ -105,6 +121,7 @@ typedef struct {
   int32_t n_weights;   /* gaussian/unsharp/log: 2*ceil(4 sigma)+1, or 0 */
   const float* weights; /* optional f32 taps from the caller's _gaussian_kernel
                            (filters.py:26-30); NULL = computed by the library */
+  const double* weights64; /* local_threshold gaussian: n_weights float64 taps */
 } hb_stage;
 
 /* One chunk of a ChunkPlan (chunking.py:93-111): interior [z_start, z_stop),

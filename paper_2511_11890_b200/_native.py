@@ -26,6 +26,9 @@ HB_U8, HB_U16, HB_U32, HB_F32 = 0, 1, 2, 3
 HB_HOST, HB_DEVICE = 0, 1
 OP_IDENTITY, OP_GAUSSIAN, OP_MEAN, OP_MEDIAN, OP_UNSHARP, OP_LOG, OP_ERODE, OP_DILATE = range(8)
 OP_HESSIAN, OP_SOBEL, OP_PREWITT, OP_THRESHOLD, OP_LBP2D, OP_DIFFUSION = range(8, 14)
+OP_LOCAL_THRESHOLD = 14
+# hb_local_kind: threshold.LOCAL_KINDS order (threshold.py:21)
+LOCAL_KINDS = ("mean", "median", "gaussian", "niblack", "sauvola")
 PREC_FAST, PREC_EXACT = 0, 1
 
 DTYPE_CODE = {
@@ -59,6 +62,7 @@ class HbStage(ctypes.Structure):
         ("offsets", ctypes.POINTER(ctypes.c_int32)),
         ("n_weights", ctypes.c_int32),
         ("weights", ctypes.POINTER(ctypes.c_float)),
+        ("weights64", ctypes.POINTER(ctypes.c_double)),
     ]
 
 
@@ -222,6 +226,7 @@ class Stage:
     radius: int = 0
     offsets: Optional[np.ndarray] = None   # (n, 3) int32
     weights: Optional[np.ndarray] = None   # float32 taps
+    weights64: Optional[np.ndarray] = None  # float64 taps (local_threshold gaussian)
 
     def halo(self) -> int:
         if self.op in (OP_GAUSSIAN, OP_UNSHARP):
@@ -230,7 +235,7 @@ class Stage:
             return (len(self.weights) - 1) // 2 + 2
         if self.op in (OP_SOBEL, OP_PREWITT):
             return 1
-        if self.op == OP_DIFFUSION:
+        if self.op in (OP_DIFFUSION, OP_LOCAL_THRESHOLD):
             return int(self.radius)
         if self.op in (OP_MEAN, OP_MEDIAN):
             return int(self.radius)
@@ -242,7 +247,7 @@ class Stage:
         if self.op in (OP_GAUSSIAN, OP_UNSHARP, OP_LOG, OP_MEAN, OP_HESSIAN, OP_SOBEL, OP_PREWITT,
                        OP_DIFFUSION):
             return np.dtype("float32")
-        if self.op == OP_THRESHOLD:
+        if self.op in (OP_THRESHOLD, OP_LOCAL_THRESHOLD):
             return np.dtype("uint32")  # LABEL_DTYPE (volume.py:23)
         if self.op == OP_LBP2D:
             return np.dtype("uint8")
@@ -290,6 +295,11 @@ class _Marshalled:
                 self._keep.append(w)
                 st.n_weights = w.size
                 st.weights = w.ctypes.data_as(ctypes.POINTER(ctypes.c_float))
+            if s.weights64 is not None:
+                w = np.ascontiguousarray(s.weights64, dtype=np.float64)
+                self._keep.append(w)
+                st.n_weights = w.size
+                st.weights64 = w.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
         self.n = n
 
 

@@ -48,6 +48,8 @@ struct StageDesc {
   std::vector<int32_t> offsets;  // reflected for dilation
   double threshold = 0.0;        // apply_threshold's t (kept in f64, NumPy semantics)
   float kappa = 0.f;             // anisotropic diffusion
+  LocalParams lt;                // local_threshold (kern set at run time)
+  std::vector<double> lt_kern;
   int in_dt = HB_F32, out_dt = HB_F32;
 };
 
@@ -179,6 +181,56 @@ hb_status normalise(const hb_stage* st, int nst, int in_dt, std::vector<StageDes
         d.precision = s.precision;
         d.out_dt = HB_F32;
         break;
+      case HB_OP_LOCAL_THRESHOLD: {  // threshold.py:188-216 validation
+        if (s.precision < HB_LT_MEAN || s.precision > HB_LT_SAUVOLA) {
+          msg = "kind must be one of ('mean', 'median', 'gaussian', 'niblack', 'sauvola'), got code " +
+                std::to_string(s.precision);
+          return HB_EPARAM;
+        }
+        if (s.radius < 1) {
+          msg = "window radius must be >= 1, got " + std::to_string(s.radius);
+          return HB_EPARAM;
+        }
+        if (s.radius > local_threshold_max_radius(s.precision, dt)) {
+          msg = "window radius " + std::to_string(s.radius) + " exceeds the device limit " +
+                std::to_string(local_threshold_max_radius(s.precision, dt)) + " for this kind and dtype";
+          return HB_EUNSUPPORTED;
+        }
+        double sauvola_r = s.amount;
+        if (s.precision == HB_LT_SAUVOLA && std::isnan(sauvola_r))  // default_sauvola_r, threshold.py:166-171
+          sauvola_r = dt == HB_U8 ? 127.5 : dt == HB_U16 ? 32767.5 : dt == HB_U32 ? 2147483647.5 : 0.5;
+        if (s.precision == HB_LT_SAUVOLA && !(sauvola_r > 0)) {
+          msg = "sauvola R must be positive, got " + std::to_string(sauvola_r);
+          return HB_EPARAM;
+        }
+        d.lt.kind = s.precision;
+        d.lt.w = s.radius;
+        d.lt.k = s.sigma;
+        d.lt.c = s.precision == HB_LT_SAUVOLA ? 0.0 : s.amount;
+        d.lt.r = s.precision == HB_LT_SAUVOLA ? sauvola_r : 1.0;
+        if (s.precision == HB_LT_GAUSSIAN) {
+          const int n = 2 * s.radius + 1;
+          d.lt_kern.resize(n);
+          if (s.weights64 && s.n_weights > 0) {
+            if (s.n_weights != n) {
+              msg = "weights64 length must be 2*window+1";
+              return HB_EPARAM;
+            }
+            std::memcpy(d.lt_kern.data(), s.weights64, sizeof(double) * n);
+          } else {  // threshold.py:199-202 (std::exp; the Python layer passes NumPy's)
+            const double sg = s.radius / 2.0;
+            for (int i = 0; i < n; i++) {
+              const double x = (double)(i - s.radius) / sg;
+              d.lt_kern[i] = std::exp(-0.5 * (x * x));
+            }
+            const double sum = pairwise_sum(d.lt_kern.data(), n);
+            for (int i = 0; i < n; i++) d.lt_kern[i] /= sum;
+          }
+        }
+        d.halo = s.radius;
+        d.out_dt = HB_U32;
+        break;
+      }
       case HB_OP_MEAN:
       case HB_OP_MEDIAN:
         if (s.radius < 1) {
@@ -327,6 +379,8 @@ size_t chain_scratch(const std::vector<StageDesc>& st, int64_t nz, int64_t ny, i
       int64_t in_n = s == 0 ? nz : (rg[s - 1].b - rg[s - 1].a);
       total += 2 * (size_t)in_n * plane * 4;
     }
+    if (st[s].op == HB_OP_LOCAL_THRESHOLD)
+      total += local_threshold_scratch(st[s].lt.kind, st[s].in_dt, n, (int64_t)plane) + 256;
     if (st[s].op == HB_OP_LOG || st[s].op == HB_OP_HESSIAN) {
       int64_t in_n = s == 0 ? nz : (rg[s - 1].b - rg[s - 1].a);
       size_t gn = (size_t)std::min<int64_t>(in_n, n + 4);
@@ -388,6 +442,14 @@ cudaError_t run_stage(const StageDesc& d, const DevIn& in, int64_t zo, int64_t n
       return threshold(in, zo, nzo, (uint32_t*)out, d.threshold, s, launches);
     case HB_OP_LBP2D:
       return lbp2d(in, zo, nzo, (uint8_t*)out, s, launches);
+    case HB_OP_LOCAL_THRESHOLD: {
+      LocalParams p = d.lt;
+      p.kern = d.lt_kern.data();
+      const size_t sb = local_threshold_scratch(p.kind, in.dt, nzo, (int64_t)plane);
+      void* scr = sb ? pa.get(sb) : nullptr;
+      if (sb && !scr) return pa.err;
+      return local_threshold(in, zo, nzo, (uint32_t*)out, p, scr, s, launches);
+    }
     case HB_OP_DIFFUSION: {
       float* b0 = (float*)pa.get((size_t)in.nz * plane * 4);
       float* b1 = (float*)pa.get((size_t)in.nz * plane * 4);

@@ -75,6 +75,18 @@ cudaError_t lbp2d(const DevIn& in, int64_t zo, int64_t nzo, uint8_t* out, cudaSt
 cudaError_t diffusion(const DevIn& in, int64_t zo, int64_t nzo, float* out, int iterations,
                       float kappa, float dt, bool rational, float* b0, float* b1, cudaStream_t s,
                       int64_t* launches);
+// local adaptive thresholds (local.cu, threshold.py:174-217) -> uint32 labels;
+// scratch: local_threshold_scratch bytes
+constexpr int kMaxLocalRadius = 50;
+struct LocalParams {
+  int kind = HB_LT_MEAN, w = 1;
+  double k = 0.2, r = 0.5, c = 0.0;
+  const double* kern = nullptr;  // gaussian kind: 2w+1 float64 taps (host)
+};
+size_t local_threshold_scratch(int kind, int dt, int64_t slices, int64_t plane);
+int local_threshold_max_radius(int kind, int dt);
+cudaError_t local_threshold(const DevIn& in, int64_t zo, int64_t nzo, uint32_t* out, const LocalParams& p,
+                            void* scratch, cudaStream_t s, int64_t* launches);
 // dtype conversion / copy (identity op, registry.py:127-133)
 cudaError_t copy_slices(const DevIn& in, int64_t zo, int64_t nzo, void* out,
                         cudaStream_t s, int64_t* launches);

@@ -138,6 +138,40 @@ def lbp2d_program() -> _native.DeviceProgram:
     return _native.DeviceProgram([_native.Stage(_native.OP_LBP2D)])
 
 
+def local_gaussian_kernel(window: int) -> np.ndarray:
+    """threshold.py:199-202: exp(-x^2 / (2 (w/2)^2)) over -w..w, normalised
+    (NumPy's own exp and pairwise sum, so the taps are the reference's)."""
+    sigma = window / 2.0
+    x = np.arange(-window, window + 1, dtype=np.float64)
+    kern = np.exp(-0.5 * (x / sigma) ** 2)
+    kern /= kern.sum()
+    return kern
+
+
+def local_threshold_program(kind, window, k=0.2, r=None, c=0.0, dtype=None) -> _native.DeviceProgram:
+    """threshold.local_threshold (threshold.py:174-217) as one device stage;
+    ``r`` None = default_sauvola_r(dtype) (threshold.py:166-171)."""
+    if kind not in _native.LOCAL_KINDS:
+        raise ParameterError(f"kind must be one of {_native.LOCAL_KINDS}, got {kind!r}")
+    if window < 1:
+        raise ParameterError(f"window radius must be >= 1, got {window}")
+    w = int(window)
+    amount = float(c)
+    if kind == "sauvola":
+        if r is None and dtype is not None:
+            from .threshold import default_sauvola_r
+
+            r = default_sauvola_r(dtype)
+        if r is not None and r <= 0:
+            raise ParameterError(f"sauvola R must be positive, got {r}")
+        # NaN = default_sauvola_r of the stage's input dtype, resolved by the library
+        amount = float("nan") if r is None else float(r)
+    return _native.DeviceProgram([_native.Stage(
+        _native.OP_LOCAL_THRESHOLD, precision=_native.LOCAL_KINDS.index(kind), radius=w,
+        sigma=float(k), amount=amount,
+        weights64=local_gaussian_kernel(w) if kind == "gaussian" else None)])
+
+
 def threshold_program(t) -> _native.DeviceProgram:
     return _native.DeviceProgram([_native.Stage(_native.OP_THRESHOLD, amount=float(t))])
 

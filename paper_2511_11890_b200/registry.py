@@ -219,6 +219,12 @@ _map("anisotropic_diffusion",
      lambda p: filters.diffusion_program(p["iterations"], p["kappa"], p["dt"], p["mode"]))
 _map("lbp2d", {}, lambda p: OpProfile(halo_z=0, scratch_factor=4, out_dtype=np.dtype("uint8")),
      lambda p: filters.lbp2d_program())
+_map("local_threshold",
+     {"kind": (str, REQUIRED), "window": (int, REQUIRED), "k": (float, 0.2),
+      "R": (lambda v: None if v is None else float(v), None), "c": (float, 0.0)},
+     lambda p: OpProfile(halo_z=p["window"], scratch_factor=24, out_dtype=LABEL_DTYPE),
+     lambda p: filters.local_threshold_program(p["kind"], p["window"], p["k"], p["R"], p["c"]),
+     output="labels")
 _map("apply_threshold", {"t": (float, REQUIRED)},
      lambda p: OpProfile(halo_z=0, scratch_factor=6, out_dtype=LABEL_DTYPE),
      lambda p: filters.threshold_program(p["t"]), output="labels")

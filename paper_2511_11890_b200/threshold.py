@@ -1,8 +1,6 @@
-"""Thresholding map operator of the drop-in API (reference threshold.py).
-
-Only the local map operator ``apply_threshold`` (threshold.py:110-112) is on
-the device path; Otsu / local thresholds are two-pass global operators,
-SURVEY.md §8(f) row 3 (not built here)."""
+"""Thresholds of the drop-in API (reference threshold.py), all on the device:
+``apply_threshold`` and ``local_threshold`` are map operators through the
+chunk executor; global Otsu is the two-pass operator of SURVEY.md §8(f) row 3."""
 
 from __future__ import annotations
 
@@ -138,3 +136,28 @@ def otsu_binarize(data, bins: int = DEFAULT_BINS, budget=None, cancel=None):
     out, _ = execute_chunked(arr, prog, OpProfile(halo_z=0, scratch_factor=6, out_dtype=LABEL_DTYPE),
                              budget, cancel=cancel, fresh_job=False)
     return out, t
+
+
+# ---------------------------------------------------------------------------
+# Local adaptive thresholds (threshold.py:166-217) — one device map stage
+# (local.cu); chunked like any map operator (halo = window).
+# ---------------------------------------------------------------------------
+LOCAL_KINDS = _native.LOCAL_KINDS
+
+
+def default_sauvola_r(dtype) -> float:
+    """Half the dtype range (127.5 for uint8); 0.5 for float data (threshold.py:166-171)."""
+    if np.issubdtype(np.dtype(dtype), np.integer):
+        info = np.iinfo(dtype)
+        return (info.max - info.min) / 2.0
+    return 0.5
+
+
+def local_threshold(data, kind: str, window: int, k: float = 0.2, r=None, c: float = 0.0):
+    """Adaptive binarization (threshold.py:174-217): labels = data > T with
+    T from the clamped (2w+1)^3 window — mean: m - c; median: med - c;
+    gaussian: gaussian-weighted mean (sigma = w/2) - c; niblack: m + k*s;
+    sauvola: m*(1 + k*(s/R - 1)); s the population std-dev."""
+    dt = data.dtype if hasattr(data, "dtype") else np.asarray(data).dtype
+    dt = np.dtype(str(dt).replace("torch.", ""))
+    return filters.apply_program(data, filters.local_threshold_program(kind, window, k, r, c, dtype=dt))

@@ -147,6 +147,15 @@ def main():
         for t in ts:
             add(f"apply_threshold_{vol}_{t}", "apply_threshold", {"t": t}, vol,
                 T.apply_threshold(vols[vol], t))
+    # local adaptive thresholds (threshold.py:174-217), every kind
+    for vol, ws in (("u8_a", (1, 2, 3)), ("u16_a", (1, 2)), ("f32_a", (1, 2)), ("f32_neg", (1, 2)),
+                    ("f32_thin", (1,))):
+        for kind in T.LOCAL_KINDS:
+            for w in ws:
+                p = {"kind": kind, "window": w, "k": 0.2 if kind != "niblack" else -0.3, "R": None,
+                     "c": 1.5 if kind in ("mean", "median", "gaussian") else 0.0}
+                add(f"local_threshold_{kind}_{vol}_{w}", "local_threshold", p, vol,
+                    T.local_threshold(vols[vol], kind, w, p["k"], p["R"], p["c"]))
     for vol in ("u8_a", "u16_a", "bin_a", "f32_neg"):
         for se in ("ball:1", "ball:2", "ball:3", "box:1", "cross:2"):
             s = M.StructuringElement.parse(se)
@@ -187,7 +196,8 @@ def main():
                          ("morph_open", {"se": "ball:3", "iterations": 2}),
                          ("identity", {}), ("hessian_xy", {"sigma": 1.5}), ("sobel", {}),
                          ("prewitt", {}), ("apply_threshold", {"t": 0.5}), ("lbp2d", {}),
-                         ("anisotropic_diffusion", {"iterations": 3, "kappa": 10.0})]:
+                         ("anisotropic_diffusion", {"iterations": 3, "kappa": 10.0}),
+                         ("local_threshold", {"kind": "sauvola", "window": 2})]:
         op = R.get_operator(name)
         pr = op.profile(R.validate_params(op, params))
         profiles[name] = {"params": params, "halo_z": pr.halo_z, "scratch": pr.scratch_factor,

@@ -48,11 +48,98 @@ def test_golden_exact_ops(hb, golden):
         if case["op"] == "mean" or (case["op"] == "anisotropic_diffusion"
                                     and case["params"]["mode"] == "exponential"):
             continue
+        if _float_box_local(case, arrays):
+            continue  # test_local_threshold_golden: float32 window sums, ulp tolerance
         got = _ours(hb, case, arrays, precision="exact")
         want = arrays[case["output"]]
         if got.dtype != want.dtype or not np.array_equal(got, want):
             bad.append(case["name"])
     assert not bad, bad
+
+
+def _float_box_local(case, arrays):
+    return (case["op"] == "local_threshold" and arrays[case["input"]].dtype == np.float32
+            and case["params"]["kind"] in ("mean", "niblack", "sauvola"))
+
+
+def _local_ok(x, got, want, t, rel=1e-12):
+    """labels equal except where data sits within rounding of T (float32 box
+    kinds: the reference's window sums are cumsum differences over the padded
+    chunk, the device's direct float64 sums — both round differently)."""
+    bad = got != want
+    if not bad.any():
+        return True
+    xv = x.astype(np.float64)[bad]
+    tv = t[bad]
+    return bool(np.all(np.abs(xv - tv) <= rel * np.maximum(1.0, np.abs(tv))))
+
+
+def test_local_threshold_golden(hb, oracle, golden):
+    """local_threshold (threshold.py:174-217), all five kinds against the
+    reference's own outputs: bit-exact for integer data and for the median /
+    gaussian kinds; float32 box kinds equal except at ulp-level ties with T."""
+    meta, arrays = golden
+    n = 0
+    for case in meta["cases"]:
+        if case["op"] != "local_threshold":
+            continue
+        n += 1
+        got = _ours(hb, case, arrays)
+        want = arrays[case["output"]]
+        assert got.dtype == want.dtype == np.uint32, case["name"]
+        if _float_box_local(case, arrays):
+            p = case["params"]
+            x = arrays[case["input"]]
+            t = oracle.local_threshold(x, p["kind"], p["window"], p["k"], p["R"], p["c"], return_t=True)
+            assert _local_ok(x, got, want, t), case["name"]
+        else:
+            assert np.array_equal(got, want), case["name"]
+    assert n >= 40
+
+
+@pytest.mark.parametrize("shape", [(40, 67, 129), (9, 1, 40), (6, 33, 7), (70, 40, 36)])
+def test_local_threshold_vs_oracle(hb, oracle, shape):
+    """every kind and dtype on ragged shapes, windows 1..4, and through a
+    tight chunk plan (integer data: bit-exact for any plan)."""
+    from paper_2511_11890_b200 import registry, threshold
+
+    rng = np.random.default_rng(sum(shape) + 3)
+    for dt in ("u8", "u16", "f32"):
+        x = _vol(rng, shape, dt)
+        for kind in threshold.LOCAL_KINDS:
+            for w in ((1, 3) if kind != "median" else (1, 2)):
+                k = 0.2 if kind != "niblack" else -0.2
+                c = 0.01 if dt == "f32" else 2.0
+                got = threshold.local_threshold(x, kind, w, k, None, c)
+                want = oracle.local_threshold(x, kind, w, k, None, c)
+                if dt == "f32" and kind in ("mean", "niblack", "sauvola"):
+                    t = oracle.local_threshold(x, kind, w, k, None, c, return_t=True)
+                    assert _local_ok(x, got, want, t), (dt, kind, w)
+                else:
+                    assert np.array_equal(got, want), (dt, kind, w)
+    # chunked: a budget that forces several chunks (halo = window)
+    x = _vol(rng, shape, "u16")
+    for kind in ("sauvola", "gaussian", "median"):
+        p = {"kind": kind, "window": 2}
+        op = registry.get_operator("local_threshold")
+        prof = op.profile(registry.validate_params(op, p))
+        out, rep = registry.run_operator(x, "local_threshold", p,
+                                         budget=budget_for(prof, x.shape, x.dtype, 4))
+        assert np.array_equal(out, oracle.local_threshold(x, kind, 2)), kind
+
+
+def test_local_threshold_errors(hb):
+    from paper_2511_11890_b200 import threshold
+    from paper_2511_11890_b200.errors import ParameterError
+
+    x = np.zeros((3, 3, 3), np.uint8)
+    with pytest.raises(ParameterError):
+        threshold.local_threshold(x, "bogus", 1)
+    with pytest.raises(ParameterError):
+        threshold.local_threshold(x, "mean", 0)
+    with pytest.raises(ParameterError):
+        threshold.local_threshold(x, "sauvola", 1, r=-1.0)
+    assert threshold.default_sauvola_r(np.uint16) == 32767.5
 
 
 def test_golden_fast_ops(hb, golden):

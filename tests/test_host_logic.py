@@ -81,7 +81,7 @@ class TestRegistry:
             "morph_erode", "morph_dilate", "morph_open", "morph_close",
             # SURVEY.md §8(f) row 2
             "hessian_xx", "hessian_yy", "hessian_zz", "hessian_xy", "hessian_xz", "hessian_yz",
-            "sobel", "prewitt", "apply_threshold", "lbp2d", "anisotropic_diffusion", "otsu",
+            "sobel", "prewitt", "apply_threshold", "local_threshold", "lbp2d", "anisotropic_diffusion", "otsu",
             "connected_components", "fill_holes", "remove_islands", "geodesic_reconstruct",
             "edt"}
 
