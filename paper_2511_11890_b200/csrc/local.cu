@@ -31,6 +31,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <type_traits>
 
 #include "ops.cuh"
@@ -148,6 +149,137 @@ k_local_box(const T* __restrict__ in, uint32_t* __restrict__ out, const LocalArg
   }
 }
 
+// Compile-time window (w <= 4): per-thread tile offsets hoisted out of the z
+// loop, the next slice's tile prefetched into registers while the current one
+// is summed, unrolled X / Y passes; integer data keeps running z sums
+// (S += new - oldest: exact mod 2^64), float data sums the ring directly.
+template <typename T, typename A1, typename A2, int WR>
+__global__ void __launch_bounds__(LT_NT)
+k_local_box_w(const T* __restrict__ in, uint32_t* __restrict__ out, const LocalArgs a) {
+  using S = typename Stage<T>::t;
+  constexpr int W = 2 * WR + 1, HT = LT_Y + 2 * WR, WT = LT_X + 2 * WR;
+  constexpr int NL = (HT * WT + LT_NT - 1) / LT_NT;  // tile loads per thread
+  constexpr int NXI = (HT + LT_Y - 1) / LT_Y;        // X-pass rows per thread
+  constexpr bool RUN = !std::is_same<A1, double>::value;
+  __shared__ S tile[HT * WT];
+  __shared__ A1 sx1[HT * LT_X];
+  __shared__ A2 sx2[HT * LT_X];
+  __shared__ A1 ring1[W * LT_NT];
+  __shared__ A2 ring2[W * LT_NT];
+  const int tid = threadIdx.x, tx = tid & (LT_X - 1), ty = tid >> 5;
+  const int x0 = blockIdx.x * LT_X, y0 = blockIdx.y * LT_Y;
+  const int o0 = blockIdx.z * a.zchunk, o1 = min(o0 + a.zchunk, a.nzo);
+  const int64_t plane = (int64_t)a.ny * a.nx;
+  int off[NL];
+#pragma unroll
+  for (int j = 0; j < NL; ++j) {
+    const int i = min(tid + j * LT_NT, HT * WT - 1);
+    const int r = i / WT, c = i - r * WT;
+    off[j] = clampi(y0 - WR + r, 0, a.ny - 1) * a.nx + clampi(x0 - WR + c, 0, a.nx - 1);
+  }
+  const int gx = x0 + tx, gy = y0 + ty;
+  const bool live = gx < a.nx && gy < a.ny;
+  const int zbeg = a.zo + o0 - WR, zend = a.zo + o1 + WR;
+  S pre[NL];
+  {
+    const T* sl = in + (int64_t)clampi(zbeg, 0, a.nz - 1) * plane;
+#pragma unroll
+    for (int j = 0; j < NL; ++j) pre[j] = (S)__ldg(sl + off[j]);
+  }
+#pragma unroll
+  for (int d = 0; d < W; ++d) {
+    ring1[d * LT_NT + tid] = A1(0);
+    ring2[d * LT_NT + tid] = A2(0);
+  }
+  A1 run1 = A1(0);
+  A2 run2 = A2(0);
+  int slot = 0;
+  for (int zi = zbeg, step = 0; zi < zend; ++zi, ++step) {
+#pragma unroll
+    for (int j = 0; j < NL; ++j)
+      if (j < NL - 1 || tid + j * LT_NT < HT * WT) tile[tid + j * LT_NT] = pre[j];
+    __syncthreads();
+    if (zi + 1 < zend) {
+      const T* sl = in + (int64_t)clampi(zi + 1, 0, a.nz - 1) * plane;
+#pragma unroll
+      for (int j = 0; j < NL; ++j) pre[j] = (S)__ldg(sl + off[j]);
+    }
+#pragma unroll
+    for (int k = 0; k < NXI; ++k) {
+      const int r = ty + k * LT_Y;
+      if (k < NXI - 1 || r < HT) {
+        const S* t = tile + r * WT + tx;
+        A1 p1 = (A1)t[0];
+        A2 p2 = sqr<A2>(t[0]);
+#pragma unroll
+        for (int d = 1; d < W; ++d) {
+          p1 = addA(p1, (A1)t[d]);
+          p2 = addA(p2, sqr<A2>(t[d]));
+        }
+        sx1[r * LT_X + tx] = p1;
+        sx2[r * LT_X + tx] = p2;
+      }
+    }
+    __syncthreads();
+    A1 q1 = sx1[ty * LT_X + tx];
+    A2 q2 = sx2[ty * LT_X + tx];
+#pragma unroll
+    for (int d = 1; d < W; ++d) {
+      q1 = addA(q1, sx1[(ty + d) * LT_X + tx]);
+      q2 = addA(q2, sx2[(ty + d) * LT_X + tx]);
+    }
+    if constexpr (RUN) {
+      run1 += q1 - ring1[slot * LT_NT + tid];
+      run2 += q2 - ring2[slot * LT_NT + tid];
+    }
+    ring1[slot * LT_NT + tid] = q1;
+    ring2[slot * LT_NT + tid] = q2;
+    slot = slot + 1 == W ? 0 : slot + 1;
+    if (step >= 2 * WR && live) {
+      A1 s1;
+      A2 s2;
+      if constexpr (RUN) {
+        s1 = run1;
+        s2 = run2;
+      } else {  // oldest first: slots slot, slot+1, ... (mod W)
+        int sl2 = slot;
+        s1 = ring1[sl2 * LT_NT + tid];
+        s2 = ring2[sl2 * LT_NT + tid];
+#pragma unroll
+        for (int d = 1; d < W; ++d) {
+          sl2 = sl2 + 1 == W ? 0 : sl2 + 1;
+          s1 = addA(s1, ring1[sl2 * LT_NT + tid]);
+          s2 = addA(s2, ring2[sl2 * LT_NT + tid]);
+        }
+      }
+      const double t = box_threshold(to_f64(s1), to_f64(s2), a);
+      const int zc = zi - WR;
+      const int64_t o = (int64_t)gy * a.nx + gx;
+      const double v = (double)__ldg(in + (int64_t)zc * plane + o);
+      __stcs(out + (int64_t)(zc - a.zo) * plane + o, v > t ? 1u : 0u);
+    }
+  }
+}
+
+template <typename T, typename A1, typename A2, int WR>
+cudaError_t run_box_w(const DevIn& in, int64_t nzo, uint32_t* out, LocalArgs a, cudaStream_t s,
+                      int64_t* launches) {
+  auto k = k_local_box_w<T, A1, A2, WR>;
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, LT_NT, 0) != cudaSuccess || per_sm < 1)
+    per_sm = 1;
+  const int gx = (int)((in.nx + LT_X - 1) / LT_X), gy = (int)((in.ny + LT_Y - 1) / LT_Y);
+  const int64_t tiles = (int64_t)gx * gy, slots = (int64_t)kNumSMs * per_sm;
+  int64_t split = std::max<int64_t>(1, (2 * slots + tiles - 1) / tiles);
+  split = std::min<int64_t>(split, std::max<int64_t>(1, nzo / std::max(8 * WR, 8)));
+  split = std::min<int64_t>(split, 65535);
+  a.zchunk = (int)((nzo + split - 1) / split);
+  dim3 grid(gx, gy, (unsigned)((nzo + a.zchunk - 1) / a.zchunk));
+  k<<<grid, LT_NT, 0, s>>>((const T*)in.p, out, a);
+  if (launches) *launches += 1;
+  return cudaGetLastError();
+}
+
 template <typename T, typename A1, typename A2>
 size_t box_smem(int w) {
   const int W = 2 * w + 1, HT = LT_Y + 2 * w, WT = LT_X + 2 * w;
@@ -158,6 +290,14 @@ size_t box_smem(int w) {
 template <typename T, typename A1, typename A2>
 cudaError_t run_box(const DevIn& in, int64_t zo, int64_t nzo, uint32_t* out, LocalArgs a, cudaStream_t s,
                     int64_t* launches) {
+  if (!std::getenv("HB_LOCAL_GENERIC")) {
+    switch (a.w) {
+      case 1: return run_box_w<T, A1, A2, 1>(in, nzo, out, a, s, launches);
+      case 2: return run_box_w<T, A1, A2, 2>(in, nzo, out, a, s, launches);
+      case 3: return run_box_w<T, A1, A2, 3>(in, nzo, out, a, s, launches);
+      case 4: return run_box_w<T, A1, A2, 4>(in, nzo, out, a, s, launches);
+    }
+  }
   const size_t smem = box_smem<T, A1, A2>(a.w);
   if (smem > 220 * 1024) return cudaErrorNotSupported;
   auto k = k_local_box<T, A1, A2>;
