@@ -284,3 +284,35 @@ def test_bench_module_mirrors_reference(tmp_path):
     assert p.read_text().splitlines() == ["size_bytes,mean_s,std_s,peak_bytes,residual_bytes", "10,0.5,0.1,7,0"]
     bench.write_csv(rows, p, device_columns=True)
     assert p.read_text().splitlines()[0].endswith("gvox_s,device_peak_bytes,device_residual_bytes,h2d_bytes,d2h_bytes")
+
+
+def _sweep_otsu_split(counts):
+    counts = counts.astype(np.float64)
+    total = counts.sum()
+    idx = np.arange(counts.size, dtype=np.float64)
+    best_split, best_sigma = None, -1.0
+    for t in range(counts.size - 1):
+        w0 = counts[: t + 1].sum()
+        w1 = total - w0
+        if w0 == 0 or w1 == 0:
+            continue
+        mu0 = (counts[: t + 1] * idx[: t + 1]).sum() / w0
+        mu1 = (counts[t + 1:] * idx[t + 1:]).sum() / w1
+        sigma = w0 * w1 * (mu0 - mu1) ** 2
+        if sigma > best_sigma:
+            best_sigma, best_split = sigma, t
+    return best_split
+
+
+def test_acceptance_criterion_04_otsu_sweep():
+    """Reference test_acceptance.py:155-188: the host Otsu finalize equals an
+    exhaustive between-class-variance sweep on 1000 random histograms."""
+    from paper_2511_11890_b200.threshold import Histogram, otsu_from_histogram
+
+    rng = np.random.default_rng(4)
+    for _ in range(1000):
+        counts = rng.integers(0, 50, size=256).astype(np.int64)
+        if np.count_nonzero(counts) < 2:
+            counts[10] += 1
+            counts[200] += 1
+        assert otsu_from_histogram(Histogram(0.0, 256.0, counts)) == float(_sweep_otsu_split(counts))
