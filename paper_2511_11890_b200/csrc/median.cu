@@ -7,6 +7,7 @@
 //           discards the min and max of the set and admits one new sample).
 // r >= 3:   per-voxel radix (bit-by-bit) selection over order-preserving keys.
 #include <algorithm>
+#include <cstdlib>
 
 #include "ops.cuh"
 #include "median_nets.h"
@@ -33,15 +34,28 @@ __device__ __forceinline__ void cs(K& a, K& b) {
   a = t;
 }
 
-// Move the minimum of a[0..m) to a[0] and the maximum to a[m-1], keeping the set.
+// Move the minimum of a[0..m) to a[0] and the maximum to a[m-1], keeping the
+// set.  Pairs (i, m-1-i) split the candidates, then two tournaments (depth
+// log2 m, same m-2 compare-exchanges as a linear scan, but independent ones
+// the scheduler can issue back to back).  With m odd the middle slot is in
+// both halves; it is always the upper index of its min-tournament pairs, so a
+// maximum parked there stays for the max tournament.
 template <int m, typename K>
 __device__ __forceinline__ void minmax_to_ends(K* a) {
 #pragma unroll
   for (int i = 0; i < m / 2; ++i) cs(a[i], a[m - 1 - i]);
 #pragma unroll
-  for (int i = 1; i <= (m - 1) / 2; ++i) cs(a[0], a[i]);
+  for (int len = (m + 1) / 2; len > 1; len = (len + 1) / 2) {
+    const int h = (len + 1) / 2;
 #pragma unroll
-  for (int i = m / 2; i < m - 1; ++i) cs(a[i], a[m - 1]);
+    for (int i = 0; i < len - h; ++i) cs(a[i], a[i + h]);
+  }
+#pragma unroll
+  for (int len = m - m / 2; len > 1; len = (len + 1) / 2) {
+    const int h = (len + 1) / 2;
+#pragma unroll
+    for (int i = 0; i < len - h; ++i) cs(a[m - 1 - i - h], a[m - 1 - i]);
+  }
 }
 
 template <typename T, typename K> struct Key;
@@ -54,16 +68,87 @@ template <typename T> struct Key<T, uint32_t> {
   static __device__ __forceinline__ T from(uint32_t k) { return (T)k; }
 };
 
+// Clamped window addressing: W slice pointers + W in-plane row offsets + W
+// column indices (~4W registers, not the W*W 64-bit row table).
 template <int W, typename T>
 struct Window {
-  const T* __restrict__ p;
-  int64_t row[W][W];  // (zc*ny + yc)*nx for each (dz, dy)
-  int64_t xc[W];
+  const T* __restrict__ sl[W];
+  int yo[W];
+  int xc[W];
   __device__ __forceinline__ T get(int e) const {
     const int a = e / (W * W), b = (e / W) % W, c = e % W;
-    return __ldg(p + row[a][b] + xc[c]);
+    return __ldg(sl[a] + yo[b] + xc[c]);
   }
 };
+
+// Two x-adjacent outputs of 8/16-bit data in one register: lo half = output x,
+// hi half = output x+1; the (data-oblivious) selection network runs on both
+// with VIMNMX.U16x2, halving its cost.
+struct U2 {
+  unsigned v;
+};
+template <> struct MinMax<U2> {
+  static __device__ __forceinline__ U2 mn(U2 a, U2 b) { return U2{__vminu2(a.v, b.v)}; }
+  static __device__ __forceinline__ U2 mx(U2 a, U2 b) { return U2{__vmaxu2(a.v, b.v)}; }
+};
+template <int W, typename T>
+struct Window2 {
+  const T* __restrict__ sl[W];
+  int yo[W];
+  int xa[W], xb[W];
+  __device__ __forceinline__ U2 get(int e) const {
+    const int a = e / (W * W), b = (e / W) % W, c = e % W;
+    const T* r = sl[a] + yo[b];
+    return U2{(unsigned)__ldg(r + xa[c]) | ((unsigned)__ldg(r + xb[c]) << 16)};
+  }
+};
+
+template <int m, int next, int N, int W, typename T>
+__device__ __forceinline__ U2 forgetful2(U2* a, const Window2<W, T>& win) {
+  minmax_to_ends<m>(a);
+  if constexpr (next < N) {
+    a[0] = win.get(next);
+    return forgetful2<m - 1, next + 1, N, W, T>(a, win);
+  } else {
+    static_assert(m == 3, "forgetful selection must end with three candidates");
+    return a[1];
+  }
+}
+
+template <int R, typename T>
+__global__ void __launch_bounds__(kThreads)
+k_median_forgetful2(const T* __restrict__ in, int64_t nz, int64_t ny, int64_t nx, int64_t zo,
+                    int64_t nzo, T* __restrict__ out) {
+  constexpr int W = 2 * R + 1;
+  constexpr int N = W * W * W;
+  constexpr int M0 = N / 2 + 2;
+  const int64_t plane = ny * nx;
+  const int64_t px = (nx + 1) / 2;
+  const int64_t total = nzo * ny * px;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = i / px;
+    const int x = (int)(i - row * px) * 2;
+    const int64_t zl = row / ny;
+    const int y = (int)(row - zl * ny);
+    const int64_t z = zl + zo;
+    Window2<W, T> win;
+#pragma unroll
+    for (int a = 0; a < W; ++a) {
+      win.sl[a] = in + clamp64(z + a - R, 0, nz - 1) * plane;
+      win.yo[a] = clampi(y + a - R, 0, (int)ny - 1) * (int)nx;
+      win.xa[a] = clampi(x + a - R, 0, (int)nx - 1);
+      win.xb[a] = clampi(x + 1 + a - R, 0, (int)nx - 1);
+    }
+    U2 a[M0];
+#pragma unroll
+    for (int e = 0; e < M0; ++e) a[e] = win.get(e);
+    const unsigned med = forgetful2<M0, M0, N, W, T>(a, win).v;
+    T* o = out + zl * plane + (int64_t)y * nx + x;
+    o[0] = (T)(med & 0xffffu);
+    if (x + 1 < nx) o[1] = (T)(med >> 16);
+  }
+}
 
 template <int m, int next, int N, int W, typename T, typename K>
 __device__ __forceinline__ K forgetful_step(K* a, const Window<W, T>& win) {
@@ -94,13 +179,11 @@ k_median_forgetful(const T* __restrict__ in, int64_t nz, int64_t ny, int64_t nx,
     int64_t x = rr - y * nx;
     int64_t z = zl + zo;
     Window<W, T> win;
-    win.p = in;
 #pragma unroll
     for (int a = 0; a < W; ++a) {
-      int64_t zc = clamp64(z + a - R, 0, nz - 1);
-#pragma unroll
-      for (int b = 0; b < W; ++b) win.row[a][b] = (zc * ny + clamp64(y + b - R, 0, ny - 1)) * nx;
-      win.xc[a] = clamp64(x + a - R, 0, nx - 1);
+      win.sl[a] = in + clamp64(z + a - R, 0, nz - 1) * plane;
+      win.yo[a] = (int)clamp64(y + a - R, 0, ny - 1) * (int)nx;
+      win.xc[a] = (int)clamp64(x + a - R, 0, nx - 1);
     }
     K a[M0];
 #pragma unroll
@@ -433,6 +516,14 @@ cudaError_t run_median(const DevIn& in, int64_t zo, int64_t nzo, void* out, int 
     k_median3_plane<T><<<grid, 256, 0, s>>>(src, in.nz, in.ny, in.nx, zo, nzo, zchunk, dst,
                                             ImadOnes{1, -1});
   } else if (r == 2) {
+    if constexpr (sizeof(T) <= 2) {
+      if (!std::getenv("HB_MEDIAN5_SCALAR")) {
+        const int g2 = grid_for(nzo * in.ny * ((in.nx + 1) / 2));
+        k_median_forgetful2<2, T><<<g2, kThreads, 0, s>>>(src, in.nz, in.ny, in.nx, zo, nzo, dst);
+        if (launches) *launches += 1;
+        return cudaGetLastError();
+      }
+    }
     k_median_forgetful<2, T, K><<<g, kThreads, 0, s>>>(src, in.nz, in.ny, in.nx, zo, nzo, dst);
   } else {
     k_median_radix<T, BITS><<<g, kThreads, 0, s>>>(src, in.nz, in.ny, in.nx, zo, nzo, dst, r);
