@@ -115,6 +115,116 @@ __device__ __forceinline__ U2 forgetful2(U2* a, const Window2<W, T>& win) {
   }
 }
 
+// ---- 5x5x5, two z-outputs per thread ---------------------------------------
+// Windows of outputs z and z+1 share C = slices z-1..z+2 (100 samples) and add
+// Ua = slice z-2 or Ub = slice z+3 (25 each).  A sample whose rank in C is
+// below 37 (above 62) has rank below (above) 62 in either window of 125, so
+// only C's middle band of ranks 37..62 (26 samples) can be a median: the band
+// comes from a forgetful trim of C (set of 64, discard min and max, admit one;
+// valid while the unseen count stays below the discards still owed on each
+// side), and each output is then the median of band ∪ U (51 samples) by the
+// usual forgetful selection.  ~1840 compare-exchanges per output instead of
+// ~3100 for the direct 125-sample selection.
+template <typename K>
+struct Get5 {  // element e of slice s (0..5 = z-2..z+3) of the 5x5 (y, x) plane
+  const void* sl[6];
+  int yo[5];
+  int xa[5], xb[5];
+};
+
+template <typename T, typename K> __device__ __forceinline__ K load5(const Get5<K>& g, int s, int e);
+template <> __device__ __forceinline__ U2 load5<uint8_t, U2>(const Get5<U2>& g, int s, int e) {
+  const uint8_t* r = (const uint8_t*)g.sl[s] + g.yo[e / 5];
+  return U2{(unsigned)__ldg(r + g.xa[e % 5]) | ((unsigned)__ldg(r + g.xb[e % 5]) << 16)};
+}
+template <> __device__ __forceinline__ U2 load5<uint16_t, U2>(const Get5<U2>& g, int s, int e) {
+  const uint16_t* r = (const uint16_t*)g.sl[s] + g.yo[e / 5];
+  return U2{(unsigned)__ldg(r + g.xa[e % 5]) | ((unsigned)__ldg(r + g.xb[e % 5]) << 16)};
+}
+template <> __device__ __forceinline__ float load5<float, float>(const Get5<float>& g, int s, int e) {
+  return __ldg((const float*)g.sl[s] + g.yo[e / 5] + g.xa[e % 5]);
+}
+template <> __device__ __forceinline__ uint32_t load5<uint32_t, uint32_t>(const Get5<uint32_t>& g, int s, int e) {
+  return __ldg((const uint32_t*)g.sl[s] + g.yo[e / 5] + g.xa[e % 5]);
+}
+
+// trim C (elements 0..99 = slices 1..4) to its middle 26 at a[1..26]
+template <int m, int next, typename T, typename K>
+__device__ __forceinline__ void trim5(K* a, const Get5<K>& g) {
+  minmax_to_ends<m>(a);
+  if constexpr (next < 100) {
+    a[0] = load5<T, K>(g, 1 + next / 25, next % 25);
+    trim5<m - 1, next + 1, T, K>(a, g);
+  } else {
+    static_assert(m == 28, "band trim must end with 28 candidates");
+  }
+}
+// median of band (26, in w[0..25]) ∪ slice s (25): w[26] = slice element 0 on entry
+template <int m, int next, typename T, typename K>
+__device__ __forceinline__ K sel51(K* a, const Get5<K>& g, int s) {
+  minmax_to_ends<m>(a);
+  if constexpr (next < 25) {
+    a[0] = load5<T, K>(g, s, next);
+    return sel51<m - 1, next + 1, T, K>(a, g, s);
+  } else {
+    static_assert(m == 3, "forgetful selection must end with three candidates");
+    return a[1];
+  }
+}
+
+template <typename T, typename K, bool PACKED>
+__global__ void __launch_bounds__(kThreads)
+k_median5_pair(const T* __restrict__ in, int64_t nz, int64_t ny, int64_t nx, int64_t zo,
+               int64_t nzo, T* __restrict__ out) {
+  const int64_t plane = ny * nx;
+  const int64_t px = PACKED ? (nx + 1) / 2 : nx;
+  const int64_t pz = (nzo + 1) / 2;
+  const int64_t total = pz * ny * px;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = i / px;
+    const int x = (int)(i - row * px) * (PACKED ? 2 : 1);
+    const int64_t zp = row / ny;
+    const int y = (int)(row - zp * ny);
+    const int64_t zl = 2 * zp, z = zl + zo;
+    Get5<K> g;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) g.sl[k] = in + clamp64(z - 2 + k, 0, nz - 1) * plane;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      g.yo[k] = clampi(y + k - 2, 0, (int)ny - 1) * (int)nx;
+      g.xa[k] = clampi(x + k - 2, 0, (int)nx - 1);
+      g.xb[k] = clampi(x + 1 + k - 2, 0, (int)nx - 1);
+    }
+    K band[64];
+#pragma unroll
+    for (int e = 0; e < 64; ++e) band[e] = load5<T, K>(g, 1 + e / 25, e % 25);
+    trim5<64, 64, T, K>(band, g);
+    K res[2];
+#pragma unroll
+    for (int o = 0; o < 2; ++o) {
+      const int sl = o == 0 ? 0 : 5;
+      K w[27];
+#pragma unroll
+      for (int j = 0; j < 26; ++j) w[j] = band[1 + j];
+      w[26] = load5<T, K>(g, sl, 0);
+      res[o] = sel51<27, 1, T, K>(w, g, sl);
+    }
+#pragma unroll
+    for (int o = 0; o < 2; ++o) {
+      if (zl + o >= nzo) break;
+      T* op = out + (zl + o) * plane + (int64_t)y * nx + x;
+      if constexpr (PACKED) {
+        const unsigned v = reinterpret_cast<const U2&>(res[o]).v;
+        op[0] = (T)(v & 0xffffu);
+        if (x + 1 < nx) op[1] = (T)(v >> 16);
+      } else {
+        op[0] = (T)res[o];
+      }
+    }
+  }
+}
+
 template <int R, typename T>
 __global__ void __launch_bounds__(kThreads)
 k_median_forgetful2(const T* __restrict__ in, int64_t nz, int64_t ny, int64_t nx, int64_t zo,
@@ -516,6 +626,16 @@ cudaError_t run_median(const DevIn& in, int64_t zo, int64_t nzo, void* out, int 
     k_median3_plane<T><<<grid, 256, 0, s>>>(src, in.nz, in.ny, in.nx, zo, nzo, zchunk, dst,
                                             ImadOnes{1, -1});
   } else if (r == 2) {
+    if (!std::getenv("HB_MEDIAN5_SINGLE")) {
+      const int64_t pairs = ((nzo + 1) / 2) * in.ny * (sizeof(T) <= 2 ? (in.nx + 1) / 2 : in.nx);
+      const int gp = grid_for(pairs);
+      if constexpr (sizeof(T) <= 2)
+        k_median5_pair<T, U2, true><<<gp, kThreads, 0, s>>>(src, in.nz, in.ny, in.nx, zo, nzo, dst);
+      else
+        k_median5_pair<T, K, false><<<gp, kThreads, 0, s>>>(src, in.nz, in.ny, in.nx, zo, nzo, dst);
+      if (launches) *launches += 1;
+      return cudaGetLastError();
+    }
     if constexpr (sizeof(T) <= 2) {
       if (!std::getenv("HB_MEDIAN5_SCALAR")) {
         const int g2 = grid_for(nzo * in.ny * ((in.nx + 1) / 2));
