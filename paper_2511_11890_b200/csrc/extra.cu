@@ -31,35 +31,35 @@ inline int grid_for(int64_t n) {
   return (int)(b < 1 ? 1 : (b < cap ? b : cap));
 }
 
+// axes are template parameters: the (z, y, x) position stays in registers
+// (a runtime-indexed int[3] lived on the stack and cost ~3x)
+template <int A, int B>
 __global__ void __launch_bounds__(kT)
 k_hessian_comp(const float* __restrict__ g, int64_t gz0, int nz, int ny, int nx, int64_t zo,
-               int64_t nzo, int axis_a, int axis_b, float* __restrict__ out) {
-  const int n[3] = {nz, ny, nx};
+               int64_t nzo, float* __restrict__ out) {
   // one output row (z, y) per block iteration: no per-voxel 64-bit division
-  for (int64_t row = blockIdx.x; row < nzo * ny; row += gridDim.x)
-  for (int x = threadIdx.x; x < nx; x += kT) {
-    const int64_t i = row * nx + x;
+  for (int64_t row = blockIdx.x; row < nzo * ny; row += gridDim.x) {
     const int zl = (int)(row / ny);
-    int p[3] = {(int)(zo + zl), (int)(row - (int64_t)zl * ny), x};
-    auto at = [&](const int (&q)[3]) {
-      return __ldg(g + ((int64_t)(q[0] - gz0) * ny + q[1]) * nx + q[2]);
-    };
-    // inner cd along a at position q (clamped per step)
-    auto cd_a = [&](int (&q)[3]) {
-      const int c = q[axis_a];
-      q[axis_a] = min(c + 1, n[axis_a] - 1);
-      const float hi = at(q);
-      q[axis_a] = max(c - 1, 0);
-      const float lo = at(q);
-      q[axis_a] = c;
-      return __fmul_rn(0.5f, __fsub_rn(hi, lo));
-    };
-    const int c = p[axis_b];
-    p[axis_b] = min(c + 1, n[axis_b] - 1);
-    const float dp = cd_a(p);
-    p[axis_b] = max(c - 1, 0);
-    const float dm = cd_a(p);
-    out[i] = __fmul_rn(0.5f, __fsub_rn(dp, dm));
+    const int z = (int)(zo + zl), y = (int)(row - (int64_t)zl * ny);
+    for (int x = threadIdx.x; x < nx; x += kT) {
+      auto at = [&](int qz, int qy, int qx) {
+        return __ldg(g + ((int64_t)(qz - gz0) * ny + qy) * nx + qx);
+      };
+      auto lim = [&](int ax) { return ax == 0 ? nz : (ax == 1 ? ny : nx); };
+      // inner cd along A at q (clamped per step), q = (qz, qy, qx)
+      auto cd_a = [&](int qz, int qy, int qx) {
+        int h[3] = {qz, qy, qx}, l[3] = {qz, qy, qx};
+        h[A] = min(h[A] + 1, lim(A) - 1);
+        l[A] = max(l[A] - 1, 0);
+        return __fmul_rn(0.5f, __fsub_rn(at(h[0], h[1], h[2]), at(l[0], l[1], l[2])));
+      };
+      int p[3] = {z, y, x}, m[3] = {z, y, x};
+      p[B] = min(p[B] + 1, lim(B) - 1);
+      m[B] = max(m[B] - 1, 0);
+      const float dp = cd_a(p[0], p[1], p[2]);
+      const float dm = cd_a(m[0], m[1], m[2]);
+      out[row * nx + x] = __fmul_rn(0.5f, __fsub_rn(dp, dm));
+    }
   }
 }
 
@@ -243,8 +243,15 @@ cudaError_t hessian_stage(const float* g, int64_t gz0, int64_t nz, int64_t ny, i
                           int64_t zo, int64_t nzo, int axis_a, int axis_b, float* out,
                           cudaStream_t s, int64_t* launches) {
   if (nzo <= 0) return cudaSuccess;
-  k_hessian_comp<<<grid_for(nzo * ny * nx), kT, 0, s>>>(g, gz0, (int)nz, (int)ny, (int)nx, zo, nzo,
-                                                         axis_a, axis_b, out);
+  const int gr = grid_for(nzo * ny * nx);
+  const int key = axis_a * 3 + axis_b;
+#define HB_HC(A, B) \
+  case A * 3 + B: k_hessian_comp<A, B><<<gr, kT, 0, s>>>(g, gz0, (int)nz, (int)ny, (int)nx, zo, nzo, out); break;
+  switch (key) {
+    HB_HC(0, 0) HB_HC(0, 1) HB_HC(0, 2) HB_HC(1, 0) HB_HC(1, 1) HB_HC(1, 2) HB_HC(2, 0) HB_HC(2, 1) HB_HC(2, 2)
+    default: return cudaErrorInvalidValue;
+  }
+#undef HB_HC
   if (launches) *launches += 1;
   return cudaGetLastError();
 }
