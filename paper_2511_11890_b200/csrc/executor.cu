@@ -380,7 +380,7 @@ size_t chain_scratch(const std::vector<StageDesc>& st, int64_t nz, int64_t ny, i
       total += 2 * (size_t)in_n * plane * 4;
     }
     if (st[s].op == HB_OP_LOCAL_THRESHOLD)
-      total += local_threshold_scratch(st[s].lt.kind, st[s].in_dt, n, (int64_t)plane) + 256;
+      total += local_threshold_scratch(st[s].lt.kind, st[s].in_dt, st[s].lt.w, n, (int64_t)plane) + 256;
     if (st[s].op == HB_OP_LOG || st[s].op == HB_OP_HESSIAN) {
       int64_t in_n = s == 0 ? nz : (rg[s - 1].b - rg[s - 1].a);
       size_t gn = (size_t)std::min<int64_t>(in_n, n + 4);
@@ -445,7 +445,7 @@ cudaError_t run_stage(const StageDesc& d, const DevIn& in, int64_t zo, int64_t n
     case HB_OP_LOCAL_THRESHOLD: {
       LocalParams p = d.lt;
       p.kern = d.lt_kern.data();
-      const size_t sb = local_threshold_scratch(p.kind, in.dt, nzo, (int64_t)plane);
+      const size_t sb = local_threshold_scratch(p.kind, in.dt, p.w, nzo, (int64_t)plane);
       void* scr = sb ? pa.get(sb) : nullptr;
       if (sb && !scr) return pa.err;
       return local_threshold(in, zo, nzo, (uint32_t*)out, p, scr, s, launches);

@@ -386,6 +386,89 @@ k_local_cmp(const T* __restrict__ data, const T* __restrict__ med, int64_t n, do
 
 inline int rows_grid(int64_t rows) { return (int)std::min<int64_t>(std::max<int64_t>(rows, 1), (int64_t)kNumSMs * 16); }
 
+// Fused gaussian kind: a 32 x 8 tile of outputs streams down z with a ring of
+// the last 2w+1 raw slices (halo'd, exact 4-byte staging) in shared memory; per
+// output slice the Z pass runs once per (y, x) of the halo'd tile, the Y pass
+// once per (y, x'), then the X pass and the comparison — the same three f64
+// folds per voxel as k_corr64 (identical operation order), without the two
+// float64 intermediate volumes (40 -> ~6 B/voxel of HBM traffic).
+template <typename T, int RC>  // RC > 0: compile-time radius (unrolled folds)
+__global__ void __launch_bounds__(LT_NT)
+k_local_gauss_tile(const T* __restrict__ in, uint32_t* __restrict__ out, int nz, int ny, int nx, int zo,
+                   int nzo, int zchunk, double c, const CorrArgs a) {
+  using S = typename Stage<T>::t;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int R = RC > 0 ? RC : a.R, W = 2 * R + 1, HT = LT_Y + 2 * R, WT = LT_X + 2 * R;
+  double* zt = reinterpret_cast<double*>(smem);  // [HT][WT]
+  double* yt = zt + HT * WT;                      // [LT_Y][WT]
+  S* ring = reinterpret_cast<S*>(yt + LT_Y * WT); // [W][HT][WT]
+  const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
+  const int x0 = blockIdx.x * LT_X, y0 = blockIdx.y * LT_Y;
+  const int o0 = blockIdx.z * zchunk, o1 = min(o0 + zchunk, nzo);
+  const int64_t plane = (int64_t)ny * nx;
+  const int TS = HT * WT;
+  auto fold = [&](auto at) {  // NI_Correlate1D order over window at(0..2R)
+    double acc;
+    if (a.sym) {
+      acc = __dmul_rn(at(R), a.w[R]);
+#pragma unroll
+      for (int d = R; d >= 1; --d) acc = __dadd_rn(acc, __dmul_rn(__dadd_rn(at(R - d), at(R + d)), a.w[R - d]));
+    } else {
+      acc = __dmul_rn(at(2 * R), a.w[2 * R]);
+#pragma unroll
+      for (int j = 0; j < 2 * R; ++j) acc = __dadd_rn(acc, __dmul_rn(at(j), a.w[j]));
+    }
+    return acc;
+  };
+  auto load = [&](int zb, S* dst) {
+    const T* sl = in + (int64_t)min(max(zb, 0), nz - 1) * plane;
+    for (int i = tid; i < TS; i += LT_NT) {
+      const int r = i / WT, cc = i - r * WT;
+      dst[i] = (S)__ldg(sl + (int64_t)min(max(y0 - R + r, 0), ny - 1) * nx + min(max(x0 - R + cc, 0), nx - 1));
+    }
+  };
+  // prime slices zo+o0-R .. zo+o0+R-1 into ring slots 0 .. 2R-1
+  for (int k = 0; k < 2 * R; ++k) load(zo + o0 - R + k, ring + k * TS);
+  int head = 2 * R;  // slot receiving the newest slice
+  const int gx = x0 + tx, gy = y0 + ty;
+  for (int o = o0; o < o1; ++o) {
+    load(zo + o + R, ring + head * TS);
+    __syncthreads();
+    const int oldest = head + 1 == W ? 0 : head + 1;  // slice zo+o-R
+    for (int i = tid; i < TS; i += LT_NT) {
+      zt[i] = fold([&](int k) {
+        int sl = oldest + k;
+        sl -= sl >= W ? W : 0;
+        return (double)ring[sl * TS + i];
+      });
+    }
+    __syncthreads();
+    for (int i = tid; i < LT_Y * WT; i += LT_NT) {
+      const int r = i / WT, cc = i - r * WT;
+      yt[i] = fold([&](int k) { return zt[(r + k) * WT + cc]; });
+    }
+    __syncthreads();
+    if (gx < nx && gy < ny) {
+      const double acc = fold([&](int k) { return yt[ty * WT + tx + k]; });
+      int ctr = oldest + R;
+      ctr -= ctr >= W ? W : 0;
+      const double v = (double)ring[ctr * TS + (ty + R) * WT + tx + R];
+      __stcs(out + (int64_t)o * plane + (int64_t)gy * nx + gx, v > __dsub_rn(acc, c) ? 1u : 0u);
+    }
+    head = oldest;
+    __syncthreads();
+  }
+}
+
+template <typename T>
+size_t gauss_tile_smem(int w) {
+  const int W = 2 * w + 1, HT = LT_Y + 2 * w, WT = LT_X + 2 * w;
+  return (size_t)HT * WT * 8 + (size_t)LT_Y * WT * 8 + (size_t)W * HT * WT * 4;
+}
+inline bool gauss_fused_ok(int w) {
+  return gauss_tile_smem<float>(w) <= 200 * 1024 && !std::getenv("HB_LOCAL_GAUSS_3PASS");
+}
+
 template <typename T>
 cudaError_t run_gauss(const DevIn& in, int64_t zo, int64_t nzo, uint32_t* out, const double* kern, int w,
                       double c, double* t0, double* t1, cudaStream_t s, int64_t* launches) {
@@ -395,9 +478,27 @@ cudaError_t run_gauss(const DevIn& in, int64_t zo, int64_t nzo, uint32_t* out, c
   a.sym = 1;  // NI_Correlate1D's symmetry test (DBL_EPSILON tolerance)
   for (int i = 1; i <= w; ++i)
     if (std::fabs(kern[w + i] - kern[w - i]) > 2.220446049250313e-16) a.sym = 0;
-  const int g = rows_grid(nzo * in.ny);
   const int nz = (int)in.nz, ny = (int)in.ny, nx = (int)in.nx;
   const T* data = (const T*)in.p;
+  const size_t smem = gauss_tile_smem<T>(w);
+  if (gauss_fused_ok(w)) {
+    auto k = w == 1 ? k_local_gauss_tile<T, 1> : w == 2 ? k_local_gauss_tile<T, 2>
+           : w == 3 ? k_local_gauss_tile<T, 3> : w == 4 ? k_local_gauss_tile<T, 4> : k_local_gauss_tile<T, 0>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, LT_NT, smem) != cudaSuccess || per_sm < 1)
+      per_sm = 1;
+    const int gx = (nx + LT_X - 1) / LT_X, gy = (ny + LT_Y - 1) / LT_Y;
+    const int64_t tiles = (int64_t)gx * gy, slots = (int64_t)kNumSMs * per_sm;
+    int64_t split = std::max<int64_t>(1, (2 * slots + tiles - 1) / tiles);
+    split = std::min<int64_t>(std::min<int64_t>(split, std::max<int64_t>(1, nzo / std::max(8 * w, 8))), 65535);
+    const int zc = (int)((nzo + split - 1) / split);
+    k<<<dim3(gx, gy, (unsigned)((nzo + zc - 1) / zc)), LT_NT, smem, s>>>(data, out, nz, ny, nx, (int)zo,
+                                                                        (int)nzo, zc, c, a);
+    if (launches) *launches += 1;
+    return cudaGetLastError();
+  }
+  const int g = rows_grid(nzo * in.ny);
   k_corr64<0, T, T><<<g, 256, 0, s>>>(data, t0, data, out, nz, ny, nx, (int)zo, (int)nzo, c, a);
   k_corr64<1, double, T><<<g, 256, 0, s>>>(t0, t1, data, out, nz, ny, nx, (int)zo, (int)nzo, c, a);
   k_corr64<2, double, T><<<g, 256, 0, s>>>(t1, nullptr, data, out, nz, ny, nx, (int)zo, (int)nzo, c, a);
@@ -455,8 +556,8 @@ cudaError_t dispatch(const DevIn& in, int64_t zo, int64_t nzo, uint32_t* out, co
 
 }  // namespace
 
-size_t local_threshold_scratch(int kind, int dt, int64_t slices, int64_t plane) {
-  if (kind == HB_LT_GAUSSIAN) return (size_t)(2 * slices * plane * 8);
+size_t local_threshold_scratch(int kind, int dt, int w, int64_t slices, int64_t plane) {
+  if (kind == HB_LT_GAUSSIAN) return gauss_fused_ok(w) ? 0 : (size_t)(2 * slices * plane * 8);
   if (kind == HB_LT_MEDIAN) return (size_t)(slices * plane * dtype_size(dt));
   return 0;
 }

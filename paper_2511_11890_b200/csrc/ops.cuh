@@ -83,7 +83,7 @@ struct LocalParams {
   double k = 0.2, r = 0.5, c = 0.0;
   const double* kern = nullptr;  // gaussian kind: 2w+1 float64 taps (host)
 };
-size_t local_threshold_scratch(int kind, int dt, int64_t slices, int64_t plane);
+size_t local_threshold_scratch(int kind, int dt, int w, int64_t slices, int64_t plane);
 int local_threshold_max_radius(int kind, int dt);
 cudaError_t local_threshold(const DevIn& in, int64_t zo, int64_t nzo, uint32_t* out, const LocalParams& p,
                             void* scratch, cudaStream_t s, int64_t* launches);
