@@ -40,10 +40,35 @@ __device__ __forceinline__ bool cc_fg(T v) {
   return MODE == CC_ZERO ? v == T(0) : v != T(0);
 }
 
+// init with the x-runs already linked: a warp covers 32 consecutive voxels;
+// a voxel joined to its left neighbour (same row, both foreground, equal
+// values for CC_SAME) points to its run's first voxel inside the warp, or to
+// the voxel left of the warp when the run enters from the previous warp.
+// Links point to smaller indices and run starts are roots, so the union-find
+// invariants hold and no x-direction union is left to do.
 template <typename T, int MODE>
-__global__ void __launch_bounds__(kCT) k_cc_init(const T* __restrict__ in, int n, int* __restrict__ lab) {
-  for (int i = blockIdx.x * kCT + threadIdx.x; i < n; i += gridDim.x * kCT)
-    lab[i] = cc_fg<T, MODE>(in[i]) ? i : -1;
+__global__ void __launch_bounds__(kCT) k_cc_init(const T* __restrict__ in, int nx, int n, int* __restrict__ lab) {
+  const int lane = threadIdx.x & 31;
+  const int warps = gridDim.x * (kCT / 32);
+  for (int base = (blockIdx.x * (kCT / 32) + (threadIdx.x >> 5)) * 32; base < n; base += warps * 32) {
+    const int i = base + lane;
+    bool fg = false, join = false;
+    if (i < n) {
+      const T v = in[i];
+      fg = cc_fg<T, MODE>(v);
+      if (fg && i % nx != 0) {
+        const T u = in[i - 1];
+        join = cc_fg<T, MODE>(u) && (MODE != CC_SAME || u == v);
+      }
+    }
+    const unsigned starts = __ballot_sync(0xffffffffu, !join);
+    const unsigned upto = starts & (0xffffffffu >> (31 - lane));  // lanes <= this one
+    if (i < n) {
+      if (!fg) lab[i] = -1;
+      else if (!join) lab[i] = i;
+      else lab[i] = upto ? base + (31 - __clz(upto)) : base - 1;
+    }
+  }
 }
 
 // find with path halving: a link is only ever rewritten while its node is a
@@ -78,6 +103,19 @@ __device__ __forceinline__ void cc_union(int* lab, int a, int b) {
   }
 }
 
+// backward (scan-order preceding) 26-neighbours, most-connected first
+__device__ constexpr int kB26[13][3] = {
+    {-1, 0, 0}, {0, -1, 0}, {0, 0, -1}, {-1, 1, 0}, {-1, -1, 0}, {-1, 0, -1}, {-1, 0, 1},
+    {0, -1, -1}, {0, -1, 1}, {-1, 1, 1}, {-1, 1, -1}, {-1, -1, 1}, {-1, -1, -1}};
+__host__ __device__ constexpr unsigned b26_adj(int k) {  // neighbours 26-adjacent to k, and k
+  unsigned m = 0;
+  for (int j = 0; j < 13; ++j) {
+    const int a = kB26[k][0] - kB26[j][0], b = kB26[k][1] - kB26[j][1], c = kB26[k][2] - kB26[j][2];
+    if (a >= -1 && a <= 1 && b >= -1 && b <= 1 && c >= -1 && c <= 1) m |= 1u << j;
+  }
+  return m;
+}
+
 template <int CONN, typename T, int MODE>
 __global__ void __launch_bounds__(kCT)
 k_cc_union(int* __restrict__ lab, const T* __restrict__ in, int nz, int ny, int nx) {
@@ -88,23 +126,36 @@ k_cc_union(int* __restrict__ lab, const T* __restrict__ in, int nz, int ny, int 
     const T vi = MODE == CC_SAME ? in[i] : T(0);
     auto linked = [&](int j) { return lab[j] >= 0 && (MODE != CC_SAME || in[j] == vi); };
     if (CONN == 6) {
-      if (x > 0 && linked(i - 1)) cc_union(lab, i, i - 1);
-      if (y > 0 && linked(i - nx)) cc_union(lab, i, i - nx);
-      if (z > 0 && linked(i - plane)) cc_union(lab, i, i - plane);
+      // x-edges are linked by k_cc_init.  A y (z) edge is implied when the left
+      // neighbours are joined the same way: i ~ i-1 ~ i-1-nx ~ i-nx, the middle
+      // edge being some voxel's own y (z) edge further left in the run.
+      const bool left = x > 0 && linked(i - 1);
+      if (y > 0 && linked(i - nx) && !(left && linked(i - 1 - nx))) cc_union(lab, i, i - nx);
+      if (z > 0 && linked(i - plane) && !(left && linked(i - 1 - plane))) cc_union(lab, i, i - plane);
     } else {
-      // the 13 neighbours that precede i in scan order
+      // The 13 neighbours that precede i in scan order, greedily: once i is
+      // linked to a neighbour A, every other neighbour B that is 26-adjacent to
+      // A needs no union of its own — A and B are linked by whichever of the
+      // two comes later in scan order (the relation is transitive for all
+      // modes: nonzero, zero, equal value).  The centre below (first in the
+      // list) is adjacent to all twelve others.
+      unsigned m = 0;
 #pragma unroll
-      for (int dz = -1; dz <= 0; ++dz)
+      for (int k = 0; k < 13; ++k) {
+        const int dz = kB26[k][0], dy = kB26[k][1], dx = kB26[k][2];
+        const int zz = z + dz, yy = y + dy, xx = x + dx;
+        if (zz < 0 || yy < 0 || yy >= ny || xx < 0 || xx >= nx) continue;
+        if (linked(i + dz * plane + dy * nx + dx)) m |= 1u << k;
+      }
+      // the x-1 neighbour is already joined by k_cc_init: free link
+      if (m & (1u << 2)) m &= ~b26_adj(2);
 #pragma unroll
-        for (int dy = -1; dy <= 1; ++dy)
-#pragma unroll
-          for (int dx = -1; dx <= 1; ++dx) {
-            if (dz == 0 && (dy > 0 || (dy == 0 && dx >= 0))) continue;
-            const int zz = z + dz, yy = y + dy, xx = x + dx;
-            if (zz < 0 || yy < 0 || yy >= ny || xx < 0 || xx >= nx) continue;
-            const int j = i + dz * plane + dy * nx + dx;
-            if (linked(j)) cc_union(lab, i, j);
-          }
+      for (int k = 0; k < 13; ++k) {
+        if (m & (1u << k)) {
+          cc_union(lab, i, i + kB26[k][0] * plane + kB26[k][1] * nx + kB26[k][2]);
+          m &= ~b26_adj(k);
+        }
+      }
     }
   }
 }
@@ -180,7 +231,7 @@ void cc_label_t(const T* in, int nz, int ny, int nx, int conn, int* lab, int* ro
                 cudaStream_t s) {
   const int n = nz * ny * nx;
   const int g = cgrid(n);
-  k_cc_init<T, MODE><<<g, kCT, 0, s>>>(in, n, lab);
+  k_cc_init<T, MODE><<<g, kCT, 0, s>>>(in, nx, n, lab);
   if (conn == 6) k_cc_union<6, T, MODE><<<g, kCT, 0, s>>>(lab, in, nz, ny, nx);
   else k_cc_union<26, T, MODE><<<g, kCT, 0, s>>>(lab, in, nz, ny, nx);
   k_cc_flatten<<<g, kCT, 0, s>>>(lab, flag, n, root);
