@@ -16,6 +16,8 @@
 // Volumes up to 2^31 - 1 voxels (int32 labels), resident in HBM.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include <cub/device/device_scan.cuh>
 
 #include "ops.cuh"
@@ -119,10 +121,13 @@ __host__ __device__ constexpr unsigned b26_adj(int k) {  // neighbours 26-adjace
 template <int CONN, typename T, int MODE>
 __global__ void __launch_bounds__(kCT)
 k_cc_union(int* __restrict__ lab, const T* __restrict__ in, int nz, int ny, int nx) {
-  const int plane = ny * nx, n = nz * plane;
-  for (int i = blockIdx.x * kCT + threadIdx.x; i < n; i += gridDim.x * kCT) {
+  const int plane = ny * nx;
+  // one (z, y) row per block iteration: no per-voxel integer division
+  for (int row = blockIdx.x; row < nz * ny; row += gridDim.x)
+  for (int x = threadIdx.x; x < nx; x += kCT) {
+    const int i = row * nx + x;
     if (lab[i] < 0) continue;
-    const int z = i / plane, r = i - z * plane, y = r / nx, x = r - y * nx;
+    const int z = row / ny, y = row - z * ny;
     const T vi = MODE == CC_SAME ? in[i] : T(0);
     auto linked = [&](int j) { return lab[j] >= 0 && (MODE != CC_SAME || in[j] == vi); };
     if (CONN == 6) {
@@ -232,8 +237,9 @@ void cc_label_t(const T* in, int nz, int ny, int nx, int conn, int* lab, int* ro
   const int n = nz * ny * nx;
   const int g = cgrid(n);
   k_cc_init<T, MODE><<<g, kCT, 0, s>>>(in, nx, n, lab);
-  if (conn == 6) k_cc_union<6, T, MODE><<<g, kCT, 0, s>>>(lab, in, nz, ny, nx);
-  else k_cc_union<26, T, MODE><<<g, kCT, 0, s>>>(lab, in, nz, ny, nx);
+  const int gr = (int)std::min<int64_t>((int64_t)nz * ny, (int64_t)kNumSMs * 64);
+  if (conn == 6) k_cc_union<6, T, MODE><<<gr, kCT, 0, s>>>(lab, in, nz, ny, nx);
+  else k_cc_union<26, T, MODE><<<gr, kCT, 0, s>>>(lab, in, nz, ny, nx);
   k_cc_flatten<<<g, kCT, 0, s>>>(lab, flag, n, root);
 }
 
