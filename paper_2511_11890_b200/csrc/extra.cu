@@ -416,12 +416,13 @@ k_geo_check(const T* __restrict__ marker, const T* __restrict__ mask, int64_t n,
 template <typename T, bool DIL>
 __global__ void __launch_bounds__(kT)
 k_geo_sweep(T* cur, const T* __restrict__ mask, int nz, int ny, int nx, int* __restrict__ changed) {
-  const int64_t plane = (int64_t)ny * nx, n = (int64_t)nz * plane;
+  const int64_t plane = (int64_t)ny * nx;
   bool any = false;
-  for (int64_t i = blockIdx.x * (int64_t)kT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kT) {
-    const int z = (int)(i / plane);
-    const int64_t rr = i - (int64_t)z * plane;
-    const int y = (int)(rr / nx), x = (int)(rr % nx);
+  // one (z, y) row per block iteration (no per-voxel 64-bit division)
+  for (int64_t row = blockIdx.x; row < (int64_t)nz * ny; row += gridDim.x)
+  for (int x = threadIdx.x; x < nx; x += kT) {
+    const int z = (int)(row / ny), y = (int)(row - (int64_t)z * ny);
+    const int64_t i = row * nx + x;
     const T v = cur[i];
     T m = v;
     auto take = [&](int64_t j) {
@@ -459,9 +460,10 @@ cudaError_t geo_t(const T* marker, const T* mask, int64_t nz, int64_t ny, int64_
   if ((const void*)out != (const void*)marker)
     cudaMemcpyAsync(out, marker, (size_t)n * sizeof(T), cudaMemcpyDeviceToDevice, s);
   int64_t k = 0;
+  const int gr = (int)std::min<int64_t>(nz * ny, (int64_t)kNumSMs * 64);
   do {
     cudaMemsetAsync(flags, 0, 4, s);
-    k_geo_sweep<T, DIL><<<g, kT, 0, s>>>(out, mask, (int)nz, (int)ny, (int)nx, flags);
+    k_geo_sweep<T, DIL><<<gr, kT, 0, s>>>(out, mask, (int)nz, (int)ny, (int)nx, flags);
     cudaMemcpyAsync(&h, flags, 4, cudaMemcpyDeviceToHost, s);
     e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) return e;
