@@ -210,14 +210,28 @@ k_fill(const T* __restrict__ in, const int* __restrict__ root, const int* __rest
 // component sizes by root; neighbouring voxels mostly share a root, so the
 // lanes of a warp with equal roots add once (__match_any_sync) instead of
 // serialising on one address (a giant component made this 2.3 Gvox/s)
+// — and the block's "hot" root (its first voxel's, usually the giant
+// component's) is counted in shared memory and added once per block
 __global__ void __launch_bounds__(kCT) k_sizes(const int* __restrict__ root, int n, int* __restrict__ size) {
+  __shared__ int hot, cnt;
+  if (threadIdx.x == 0) {
+    hot = blockIdx.x * kCT < n ? root[blockIdx.x * kCT] : -1;
+    cnt = 0;
+  }
+  __syncthreads();
+  const int h = hot;
   for (int i0 = blockIdx.x * kCT; i0 < n; i0 += gridDim.x * kCT) {
     const int i = i0 + threadIdx.x;
     const int r = i < n ? root[i] : -1;
     const unsigned peers = __match_any_sync(0xffffffffu, r);
     const int leader = __ffs(peers) - 1;
-    if (r >= 0 && (int)(threadIdx.x & 31) == leader) atomicAdd(&size[r], __popc(peers));
+    if (r >= 0 && (int)(threadIdx.x & 31) == leader) {
+      if (r == h) atomicAdd(&cnt, __popc(peers));
+      else atomicAdd(&size[r], __popc(peers));
+    }
   }
+  __syncthreads();
+  if (threadIdx.x == 0 && h >= 0 && cnt) atomicAdd(&size[h], cnt);
 }
 
 template <typename T>
