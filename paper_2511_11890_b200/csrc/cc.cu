@@ -144,22 +144,25 @@ k_cc_union(int* __restrict__ lab, const T* __restrict__ in, int nz, int ny, int 
       // two comes later in scan order (the relation is transitive for all
       // modes: nonzero, zero, equal value).  The centre below (first in the
       // list) is adjacent to all twelve others.
-      unsigned m = 0;
+      // Neighbours are loaded lazily, in priority order, only while some are
+      // still uncovered (the centre below alone covers all twelve others).
+      unsigned todo = (1u << 13) - 1;
+      // the x-1 neighbour is already joined by k_cc_init: a free link
+      if (x > 0 && linked(i - 1)) todo &= ~b26_adj(2);
+      todo &= ~(1u << 2);
 #pragma unroll
       for (int k = 0; k < 13; ++k) {
+        if (k == 2 || !(todo & (1u << k))) continue;
         const int dz = kB26[k][0], dy = kB26[k][1], dx = kB26[k][2];
         const int zz = z + dz, yy = y + dy, xx = x + dx;
-        if (zz < 0 || yy < 0 || yy >= ny || xx < 0 || xx >= nx) continue;
-        if (linked(i + dz * plane + dy * nx + dx)) m |= 1u << k;
-      }
-      // the x-1 neighbour is already joined by k_cc_init: free link
-      if (m & (1u << 2)) m &= ~b26_adj(2);
-#pragma unroll
-      for (int k = 0; k < 13; ++k) {
-        if (m & (1u << k)) {
-          cc_union(lab, i, i + kB26[k][0] * plane + kB26[k][1] * nx + kB26[k][2]);
-          m &= ~b26_adj(k);
+        const int j = i + dz * plane + dy * nx + dx;
+        if (zz >= 0 && yy >= 0 && yy < ny && xx >= 0 && xx < nx && linked(j)) {
+          cc_union(lab, i, j);
+          todo &= ~b26_adj(k);
+        } else {
+          todo &= ~(1u << k);
         }
+        if (!todo) break;
       }
     }
   }
