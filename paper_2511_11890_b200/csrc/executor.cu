@@ -775,8 +775,8 @@ int32_t cc_chunked(const hb_volume* in, hb_volume* out, int conn, int dev, int64
     cz = std::min(cs, nz - z0);
     const size_t bytes = (size_t)(cz * plane) * es;
     const char* src = (const char*)in->data + (size_t)(z0 * plane) * es;
-    return cudaMemcpyAsync(d_in, src, bytes, in->location == HB_DEVICE ? cudaMemcpyDeviceToDevice
-                                                                           : cudaMemcpyHostToDevice, s);
+    return in->location == HB_DEVICE ? cudaMemcpyAsync(d_in, src, bytes, cudaMemcpyDeviceToDevice, s)
+                                     : h2d_any(dev, d_in, src, bytes, s);
   };
   // pass 1: per-chunk candidates + boundary unions
   for (int64_t c = 0; c < nchunks && e == cudaSuccess; ++c) {
@@ -833,8 +833,7 @@ int32_t cc_chunked(const hb_volume* in, hb_volume* out, int conn, int dev, int64
     uint32_t* dst = out->location == HB_DEVICE ? (uint32_t*)out->data + c * cs * plane : d_out;
     if (e == cudaSuccess) e = cc_apply_table(rank, (int)(cz * plane), table, dst, s);
     if (e == cudaSuccess && out->location != HB_DEVICE)
-      e = cudaMemcpyAsync((uint32_t*)out->data + c * cs * plane, d_out, (size_t)(cz * plane) * 4,
-                          cudaMemcpyDeviceToHost, s);
+      e = d2h_any(dev, (uint32_t*)out->data + c * cs * plane, d_out, (size_t)(cz * plane) * 4, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // the host table slice / d_out are reused
   }
   cudaStreamSynchronize(s);
