@@ -593,6 +593,188 @@ k_median3_plane(const T* __restrict__ in, int64_t nz, int64_t ny, int64_t nx, in
   }
 }
 
+// ---------------------------------------------------------------------------
+// 3x3x3 median of 8/16-bit data: the same plane / merge / select networks on
+// two x-adjacent outputs packed per 32-bit register (lo half = x, hi half =
+// x+1): min/max are VIMNMX(3).U16x2, and the max = a + b - min identity stays
+// exact lane-wise (the 32-bit result is the packed maxima mod 2^32).  One
+// plane network per output pair instead of planes2's shared-triple pair, one
+// merge and one select per pair.
+// ---------------------------------------------------------------------------
+struct NetP {
+  ImadOnes c;
+  static __device__ __forceinline__ int mn(int a, int b) { return (int)__vminu2((unsigned)a, (unsigned)b); }
+  static __device__ __forceinline__ int mx(int a, int b) { return (int)__vmaxu2((unsigned)a, (unsigned)b); }
+  __device__ __forceinline__ void ce(int& a, int& b) const {
+    const int lo = mn(a, b);
+    const int s = imad(a, c.one, b);
+    b = imad(lo, c.mone, s);
+    a = lo;
+  }
+  __device__ __forceinline__ void sort3(int& a, int& b, int& cc) const {
+    const int lo = mn(a, mn(b, cc));
+    const int hi = mx(a, mx(b, cc));
+    int t = imad(a, c.one, b);
+    t = imad(cc, c.one, t);
+    t = imad(lo, c.mone, t);
+    b = imad(hi, c.mone, t);
+    a = lo;
+    cc = hi;
+  }
+  __device__ __forceinline__ void tableau(const int (&m)[3][3], int (&s)[9]) const {
+    s[0] = m[0][0]; s[1] = m[0][1]; s[2] = m[1][0]; s[3] = m[0][2]; s[4] = m[1][1];
+    s[5] = m[2][0]; s[6] = m[1][2]; s[7] = m[2][1]; s[8] = m[2][2];
+    ce(s[3], s[5]); ce(s[1], s[2]); ce(s[2], s[3]); ce(s[6], s[7]);
+    ce(s[5], s[6]); ce(s[3], s[4]); ce(s[4], s[5]);
+  }
+  // packed plane of the output pair from r[row][x-1..x+2] (16-bit keys)
+  __device__ __forceinline__ void plane(const int (&r)[3][4], int (&p)[9]) const {
+    int m[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) m[i][j] = (int)__byte_perm((unsigned)r[i][j], (unsigned)r[i][j + 1], 0x5410);
+#pragma unroll
+    for (int j = 0; j < 3; ++j) sort3(m[0][j], m[1][j], m[2][j]);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) sort3(m[i][0], m[i][1], m[i][2]);
+    tableau(m, p);
+  }
+  __device__ __forceinline__ void merge(const int (&cur)[9], const int (&nxt)[9], int (&m)[10]) const {
+    int w[18];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) {
+      w[i] = cur[i];
+      w[9 + i] = nxt[i];
+    }
+#define HB_CE(i, j) ce(w[i], w[j]);
+#define HB_MN(i, j) w[i] = mn(w[i], w[j]);
+#define HB_MX(i, j) w[j] = mx(w[i], w[j]);
+    HB_MERGE9_RANK4_13(HB_CE, HB_MN, HB_MX)
+#undef HB_CE
+#undef HB_MN
+#undef HB_MX
+#pragma unroll
+    for (int i = 0; i < 10; ++i) m[i] = w[4 + i];
+  }
+  __device__ __forceinline__ int select(const int (&m)[10], const int (&p)[9]) const {
+    const int t0 = m[9];
+    const int t1 = mx(m[8], p[0]);
+    const int t2 = mx(m[7], p[1]);
+    const int t3 = mx(m[6], p[2]);
+    const int t4 = mx(m[5], p[3]);
+    const int t5 = mx(m[4], p[4]);
+    const int t6 = mx(m[3], p[5]);
+    const int t7 = mx(m[2], p[6]);
+    const int t8 = mx(m[1], p[7]);
+    const int t9 = mx(m[0], p[8]);
+    int r = mn(t0, mn(t1, t2));
+    r = mn(r, mn(t3, t4));
+    r = mn(r, mn(t5, t6));
+    r = mn(r, mn(t7, t8));
+    return mn(r, t9);
+  }
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256, 3)
+k_median3_packed(const T* __restrict__ in, int64_t nz, int64_t ny, int64_t nx, int64_t zo,
+                 int64_t nzo, int zchunk, T* __restrict__ out, ImadOnes ones) {
+  __shared__ __align__(16) int tile[3][M3_H][M3_W];
+  const NetP net{ones};
+  const int tid = threadIdx.x;
+  const int tx = tid & 31, ty = tid >> 5;
+  const int64_t x0 = (int64_t)blockIdx.x * M3_TX, y0 = (int64_t)blockIdx.y * M3_TY;
+  const int zs = (int)blockIdx.z * zchunk;
+  const int ze = min(zs + zchunk, (int)nzo);
+  constexpr int NE = M3_H * M3_W;
+  constexpr int PER = (NE + 255) / 256;
+  int goff[PER];
+  bool gval[PER];
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const int e = tid + 256 * k;
+    gval[k] = e < NE;
+    const int ly = gval[k] ? e / M3_W : 0, lx = gval[k] ? e % M3_W : 0;
+    const int64_t gy = clamp64(y0 - 1 + ly, 0, ny - 1), gx = clamp64(x0 - 1 + lx, 0, nx - 1);
+    goff[k] = (int)(gy * nx + gx);
+  }
+  const int64_t plane = ny * nx;
+  const int zlast = (int)nz - 1;
+  auto slice_ptr = [&](int zb) { return in + (int64_t)min(max(zb, 0), zlast) * plane; };
+  auto fetch = [&](const T* src, T (&v)[PER]) {
+#pragma unroll
+    for (int k = 0; k < PER; ++k) v[k] = gval[k] ? __ldg(src + goff[k]) : T(0);
+  };
+  auto stash = [&](int* buf, const T (&v)[PER]) {
+#pragma unroll
+    for (int k = 0; k < PER; ++k)
+      if (gval[k]) buf[tid + 256 * k] = (int)v[k];
+  };
+  auto planes = [&](const int* buf, int (&p)[9]) {
+    int r[3][4];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const int2 lo = *reinterpret_cast<const int2*>(buf + (ty + i) * M3_W + 2 * tx);
+      const int2 hi = *reinterpret_cast<const int2*>(buf + (ty + i) * M3_W + 2 * tx + 2);
+      r[i][0] = lo.x; r[i][1] = lo.y; r[i][2] = hi.x; r[i][3] = hi.y;
+    }
+    net.plane(r, p);
+  };
+  const int64_t gy = y0 + ty, gx = x0 + 2 * tx;
+  const bool st_y = gy < ny, st_x0 = gx < nx, st_x1 = gx + 1 < nx;
+  T* optr = out + (int64_t)zs * plane + gy * nx + gx;
+  auto emit = [&](int k) {
+    if (st_y) {
+      if (st_x0) optr[0] = (T)(k & 0xffff);
+      if (st_x1) optr[1] = (T)((unsigned)k >> 16);
+    }
+    optr += plane;
+  };
+  int X[9], Y[9], Z[9], W[9], M[10];
+  T v[PER];
+  int* const tb0 = &tile[0][0][0];
+  constexpr int TPITCH = M3_H * M3_W;
+  const int zb0 = (int)zo + zs;
+  fetch(slice_ptr(zb0 - 1), v);
+  stash(tb0, v);
+  fetch(slice_ptr(zb0), v);
+  stash(tb0 + TPITCH, v);
+  int zf = zb0 + 1;
+  const T* pf = slice_ptr(zf);
+  fetch(pf, v);
+  __syncthreads();
+  planes(tb0, X);
+  planes(tb0 + TPITCH, Y);
+  int z = zs;
+  int* tb = tb0 + 2 * TPITCH;
+  auto next_plane = [&](int (&p)[9]) {
+    stash(tb, v);
+    ++zf;
+    if (zf <= zlast && zf > 0) pf += plane;
+    fetch(pf, v);
+    __syncthreads();
+    planes(tb, p);
+    tb = (tb == tb0 + 2 * TPITCH) ? tb0 : tb + TPITCH;
+  };
+  while (z < ze) {
+    next_plane(Z);
+    net.merge(Y, Z, M);
+    emit(net.select(M, X));
+    if (++z >= ze) break;
+    next_plane(W);
+    emit(net.select(M, W));
+    if (++z >= ze) break;
+    next_plane(X);
+    net.merge(W, X, M);
+    emit(net.select(M, Z));
+    if (++z >= ze) break;
+    next_plane(Y);
+    emit(net.select(M, Y));
+    ++z;
+  }
+}
+
 inline int grid_for(int64_t n) {
   int64_t b = (n + kThreads - 1) / kThreads;
   int64_t cap = (int64_t)kNumSMs * 16;
@@ -623,6 +805,14 @@ cudaError_t run_median(const DevIn& in, int64_t zo, int64_t nzo, void* out, int 
       }
     }
     grid.z = (unsigned)((nzo + zchunk - 1) / zchunk);
+    if constexpr (sizeof(T) <= 2) {
+      if (!std::getenv("HB_MEDIAN3_UNPACKED")) {
+        k_median3_packed<T><<<grid, 256, 0, s>>>(src, in.nz, in.ny, in.nx, zo, nzo, zchunk, dst,
+                                                 ImadOnes{1, -1});
+        if (launches) *launches += 1;
+        return cudaGetLastError();
+      }
+    }
     k_median3_plane<T><<<grid, 256, 0, s>>>(src, in.nz, in.ny, in.nx, zo, nzo, zchunk, dst,
                                             ImadOnes{1, -1});
   } else if (r == 2) {
