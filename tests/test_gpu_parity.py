@@ -128,6 +128,20 @@ def test_local_threshold_vs_oracle(hb, oracle, shape):
         assert np.array_equal(out, oracle.local_threshold(x, kind, 2)), kind
 
 
+def test_local_threshold_wide_windows(hb, oracle):
+    """windows past the compile-time kernels (w > 4: runtime-window box and
+    gaussian kernels), integer data bit-exact."""
+    from paper_2511_11890_b200 import threshold
+
+    rng = np.random.default_rng(17)
+    for dt, shape in (("u8", (14, 23, 41)), ("u16", (12, 19, 37))):
+        x = _vol(rng, shape, dt)
+        for kind in ("mean", "niblack", "sauvola", "gaussian"):
+            for w in (5, 7):
+                got = threshold.local_threshold(x, kind, w, 0.2, None, 1.0)
+                assert np.array_equal(got, oracle.local_threshold(x, kind, w, 0.2, None, 1.0)), (dt, kind, w)
+
+
 def test_local_threshold_errors(hb):
     from paper_2511_11890_b200 import threshold
     from paper_2511_11890_b200.errors import ParameterError
