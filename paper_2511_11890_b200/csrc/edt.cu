@@ -11,6 +11,7 @@
 #include <math_constants.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "ops.cuh"
 
@@ -98,6 +99,33 @@ k_edt_axis(const double* __restrict__ f, double* __restrict__ out, int nz, int n
   }
 }
 
+// (z, a, b) -> (z, b, a) transpose of float64 planes through a 32 x 33 tile;
+// with SQRT the float32 sqrt of the distance is written instead (fused final
+// step).  The x-axis scan runs on the transposed block, where its lines are
+// the middle axis (coalesced across threads, like the y scan).
+template <typename To, bool SQRT>
+__global__ void __launch_bounds__(256)
+k_edt_transpose(const double* __restrict__ in, To* __restrict__ out, int na, int nb) {
+  __shared__ double t[32][33];
+  const int z = blockIdx.z;
+  const int a0 = blockIdx.y * 32, b0 = blockIdx.x * 32;
+  const double* src = in + (int64_t)z * na * nb;
+  To* dst = out + (int64_t)z * na * nb;
+  for (int r = threadIdx.y; r < 32; r += 8) {
+    const int a = a0 + r, b = b0 + threadIdx.x;
+    if (a < na && b < nb) t[r][threadIdx.x] = src[(int64_t)a * nb + b];
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += 8) {
+    const int b = b0 + r, a = a0 + threadIdx.x;
+    if (a < na && b < nb) {
+      const double v = t[threadIdx.x][r];
+      if constexpr (SQRT) dst[(int64_t)b * na + a] = (To)__dsqrt_rn(v);
+      else dst[(int64_t)b * na + a] = (To)v;
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256) k_edt_sqrt(const double* __restrict__ d2, int64_t n, float* __restrict__ out) {
   for (int64_t i = blockIdx.x * 256ll + threadIdx.x; i < n; i += (int64_t)gridDim.x * 256)
     out[i] = (float)__dsqrt_rn(d2[i]);
@@ -128,16 +156,31 @@ cudaError_t edt(const void* in, int dt, int64_t nz, int64_t ny, int64_t nx, cons
   const int64_t lines[3] = {ny * nx, nz * nx, nz * ny};
   double* src = d2a;
   double* dst = d2b;
-  for (int axis = 0; axis < 3; ++axis) {
-    int* vbuf = reinterpret_cast<int*>(work);
-    double* zbuf = reinterpret_cast<double*>(reinterpret_cast<char*>(work) + ((size_t)n * 4 + 255) / 256 * 256);
+  int* vbuf = reinterpret_cast<int*>(work);
+  double* zbuf = reinterpret_cast<double*>(reinterpret_cast<char*>(work) + ((size_t)n * 4 + 255) / 256 * 256);
+  const bool transpose_x = nz <= 65535 && !std::getenv("HB_EDT_DIRECT_X");
+  for (int axis = 0; axis < (transpose_x ? 2 : 3); ++axis) {
     const int64_t nl = lines[axis];
     k_edt_axis<<<(unsigned)((nl + kET - 1) / kET), kET, 0, s>>>(src, dst, (int)nz, (int)ny, (int)nx, axis,
                                                                 spacing[axis], nl, vbuf, zbuf);
     std::swap(src, dst);
   }
-  if (squared) return cudaMemcpyAsync(out, src, (size_t)n * 8, cudaMemcpyDeviceToDevice, s);
-  k_edt_sqrt<<<g, 256, 0, s>>>(src, n, (float*)out);
+  if (!transpose_x) {
+    if (squared) return cudaMemcpyAsync(out, src, (size_t)n * 8, cudaMemcpyDeviceToDevice, s);
+    k_edt_sqrt<<<g, 256, 0, s>>>(src, n, (float*)out);
+    return cudaGetLastError();
+  }
+  // x scan on the (z, x, y) transpose: same per-line arithmetic, coalesced
+  const dim3 tb(32, 8);
+  k_edt_transpose<double, false><<<dim3((unsigned)((nx + 31) / 32), (unsigned)((ny + 31) / 32), (unsigned)nz), tb, 0, s>>>(
+      src, dst, (int)ny, (int)nx);
+  std::swap(src, dst);
+  k_edt_axis<<<(unsigned)((lines[2] + kET - 1) / kET), kET, 0, s>>>(src, dst, (int)nz, (int)nx, (int)ny, 1,
+                                                                    spacing[2], lines[2], vbuf, zbuf);
+  std::swap(src, dst);
+  const dim3 gb((unsigned)((ny + 31) / 32), (unsigned)((nx + 31) / 32), (unsigned)nz);
+  if (squared) k_edt_transpose<double, false><<<gb, tb, 0, s>>>(src, (double*)out, (int)nx, (int)ny);
+  else k_edt_transpose<float, true><<<gb, tb, 0, s>>>(src, (float*)out, (int)nx, (int)ny);
   return cudaGetLastError();
 }
 
