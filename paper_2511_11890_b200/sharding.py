@@ -172,6 +172,101 @@ def otsu_sharded(local, bins: int, rank: int, world: int, group=None,
     return apply_fn(local, t), t
 
 
+def connected_components_sharded(local, connectivity: int, rank: int, world: int, group=None,
+                                 label_fn: Optional[Callable] = None):
+    """Return (labels of this rank's slab, total count) — identical to the
+    single-volume connected_components (quantify.py:60-111: canonical ids in
+    first-voxel scan order) for z-slabs in rank order.
+
+    The reference's chunked scheme with ranks as chunks: each rank labels its
+    slab on its GPU (``label_fn``, default quantify.connected_components: ids
+    1..k in slab scan order = globally ordered candidates after a rank
+    offset); one all_gather carries every rank's count and its first / last
+    label planes (the path's only exchange); every rank then runs the same
+    boundary union-find over the candidates (smaller id wins) and relabels
+    its slab through the resulting table — no further communication."""
+    import torch
+
+    from . import quantify
+
+    if connectivity not in (6, 26):
+        raise ValueError(f"connectivity must be 6 or 26, got {connectivity}")
+    label_fn = label_fn or (lambda a, c: quantify.connected_components(a, c))
+    lab, k = label_fn(local, connectivity)
+    is_torch = hasattr(lab, "device") and hasattr(lab, "cpu")
+    lab_h = lab.cpu().numpy() if is_torch else np.asarray(lab)
+    nz, ny, nx = lab_h.shape
+    first = lab_h[0].astype(np.int64) if nz else np.zeros((ny, nx), np.int64)
+    last = lab_h[-1].astype(np.int64) if nz else np.zeros((ny, nx), np.int64)
+    counts = [int(k)]
+    firsts, lasts, nzs = [first], [last], [nz]
+    if world > 1:
+        dist = _dist()
+        dev = _comm_device(group)
+        meta = torch.tensor([int(k), nz], dtype=torch.int64, device=dev)
+        metas = [torch.empty_like(meta) for _ in range(world)]
+        dist.all_gather(metas, meta, group=group)
+        planes = torch.from_numpy(np.stack([first, last])).to(dev)
+        allp = [torch.empty_like(planes) for _ in range(world)]
+        dist.all_gather(allp, planes, group=group)
+        counts = [int(m[0].item()) for m in metas]
+        nzs = [int(m[1].item()) for m in metas]
+        firsts = [p[0].cpu().numpy() for p in allp]
+        lasts = [p[1].cpu().numpy() for p in allp]
+    offs = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+    parent = np.arange(int(offs[-1]), dtype=np.int64)
+
+    def find(a):
+        root = a
+        while parent[root] != root:
+            root = parent[root]
+        while parent[a] != root:
+            parent[a], a = root, parent[a]
+        return root
+
+    shifts = [(0, 0)] if connectivity == 6 else [(dy, dx) for dy in (-1, 0, 1) for dx in (-1, 0, 1)]
+    prev = None  # last non-empty slab below: (rank, its last plane)
+    for r in range(len(counts)):
+        if nzs[r] == 0:
+            continue
+        if prev is not None:
+            pr, below = prev
+            above = firsts[r]
+            for dy, dx in shifts:
+                # voxel (y, x) of the upper slab's first plane touches (y+dy, x+dx) below
+                ys = slice(max(0, -dy), ny - max(0, dy))
+                xs = slice(max(0, -dx), nx - max(0, dx))
+                yb = slice(max(0, dy), ny - max(0, -dy))
+                xb = slice(max(0, dx), nx - max(0, -dx))
+                a = above[ys, xs].ravel()
+                b = below[yb, xb].ravel()
+                both = (a > 0) & (b > 0)
+                for u, v in np.unique(np.stack([offs[pr] + b[both] - 1, offs[r] + a[both] - 1], 1), axis=0):
+                    ru, rv = find(int(u)), find(int(v))
+                    if ru != rv:
+                        parent[max(ru, rv)] = min(ru, rv)
+        prev = (r, lasts[r])
+    # final ids in candidate order (= global first-voxel order): links point to
+    # smaller ids, so pointer jumping reaches every root; roots numbered in order
+    while True:
+        nxt = parent[parent]
+        if np.array_equal(nxt, parent):
+            break
+        parent = nxt
+    is_root = parent == np.arange(parent.size)
+    ids = np.cumsum(is_root).astype(np.uint32)
+    fin = ids[parent] if parent.size else np.zeros(0, np.uint32)
+    total = int(is_root.sum())
+    mine = fin[offs[rank]:offs[rank + 1]]
+    table = np.concatenate([[0], mine]).astype(np.uint32)
+    if is_torch:
+        t = torch.from_numpy(table.astype(np.int64)).to(lab.device)
+        out = t[lab.to(torch.int64)].to(lab.dtype)
+    else:
+        out = table[lab_h]
+    return out, total
+
+
 def _comm_device(group):
     import torch
 

@@ -639,3 +639,16 @@ def test_pipelines_of_next_ops(hb, oracle, steps):
     got, rep = registry.run_pipeline(x, steps, budget_for(OpProfile(halo, 12), x.shape, x.dtype, 6))
     assert rep.chunk_count >= 3
     assert got.dtype == want.dtype and np.array_equal(got, want)
+
+
+def test_connected_components_sharded_single_rank_device(hb, oracle):
+    """sharding.connected_components_sharded on a CUDA slab (world 1): the
+    device labelling plus the on-device table gather give the canonical labels."""
+    import torch
+
+    from paper_2511_11890_b200 import sharding
+
+    m = (np.random.default_rng(5).random((30, 41, 37)) < 0.4).astype(np.uint8)
+    want, n = oracle.connected_components(m, 26)
+    got, total = sharding.connected_components_sharded(torch.from_numpy(m).cuda(), 26, 0, 1)
+    assert total == n and np.array_equal(got.cpu().numpy(), want)

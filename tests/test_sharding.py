@@ -160,3 +160,37 @@ def test_otsu_sharded_equals_whole(kind, oracle):
         ts = [float(np.load(os.path.join(d, f"t{r}.npy"))[0]) for r in range(world)]
     assert ts == [t_whole] * world
     assert np.array_equal(got, oracle.apply_threshold(vol, t_whole))
+
+
+def _cc_worker(rank, world, port, conn, outdir):
+    sys.path.insert(0, ROOT)
+    from oracle import oracle as O
+    from paper_2511_11890_b200 import sharding
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    try:
+        vol = (np.random.default_rng(31).random((23, 17, 19)) < 0.35).astype(np.uint8)
+        me = sharding.partition(vol.shape[0], world)[rank]
+        local = np.ascontiguousarray(vol[me.z0:me.z1])
+        labels, total = sharding.connected_components_sharded(
+            local, conn, rank, world, label_fn=lambda a, c: O.connected_components(a, c))
+        np.save(os.path.join(outdir, f"cc{rank}.npy"), labels)
+        np.save(os.path.join(outdir, f"n{rank}.npy"), np.array([total]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,conn", [(2, 6), (3, 26), (3, 6)])
+def test_connected_components_sharded_equals_whole(world, conn, oracle):
+    """Ranks label their z-slabs, all_gather counts and boundary planes, and
+    run the same boundary union-find: the stitched labels are the canonical
+    single-volume labels (first-voxel scan order), bit for bit."""
+    vol = (np.random.default_rng(31).random((23, 17, 19)) < 0.35).astype(np.uint8)
+    want, n = oracle.connected_components(vol, conn)
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_cc_worker, args=(world, _free_port(), conn, d), nprocs=world, join=True)
+        got = np.concatenate([np.load(os.path.join(d, f"cc{r}.npy")) for r in range(world)])
+        ns = [int(np.load(os.path.join(d, f"n{r}.npy"))[0]) for r in range(world)]
+    assert ns == [n] * world
+    assert np.array_equal(got.astype(np.uint32), want)
