@@ -162,6 +162,17 @@ const char* hb_version(void);
 int32_t hb_device_info(int32_t dev, int64_t* free_bytes, int64_t* total_bytes);
 int32_t hb_device_count(void);
 
+/* Chunk planning for C callers: plan_chunks (chunking.py:135-174), same
+ * formula and error.  t = floor(usable / (scratch_factor * slice_bytes))
+ * padded slices; t <= 2*halo -> HB_EBUDGET_SMALL with *minimum_bytes =
+ * ceil((2*halo + 1) * scratch_factor * slice_bytes); else interior n = t - 2*halo
+ * and chunks [k*n, min((k+1)*n, nz)) with halos min(halo, z_start),
+ * min(halo, nz - z_stop).  *nchunks receives the count; chunks (capacity
+ * entries, may be NULL) receives them when it is large enough. */
+int32_t hb_plan(int64_t nz, int64_t ny, int64_t nx, int32_t itemsize, int64_t halo,
+                double scratch_factor, int64_t usable_bytes, hb_chunk* chunks, int64_t capacity,
+                int64_t* nchunks, int64_t* minimum_bytes);
+
 /* Parameter helpers ------------------------------------------------------- */
 /* ceil(4*sigma) (filters.py:21-23) */
 int32_t hb_gaussian_radius(double sigma);

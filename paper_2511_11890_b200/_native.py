@@ -116,7 +116,7 @@ EXPORTS = (
     "hb_apply_device", "hb_chain_out_dtype", "hb_trim_device",
     "hb_device_pool_bytes", "hb_pin", "hb_unpin", "hb_last_error",
     "hb_session_begin", "hb_session_end", "hb_minmax", "hb_histogram",
-    "hb_connected_components", "hb_label_filter", "hb_geodesic", "hb_edt",
+    "hb_connected_components", "hb_label_filter", "hb_geodesic", "hb_edt", "hb_plan",
 )
 
 _lock = threading.Lock()

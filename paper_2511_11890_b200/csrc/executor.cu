@@ -11,7 +11,9 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <climits>
 #include <cmath>
+#include <cstdint>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -866,6 +868,43 @@ int32_t hb_device_count(void) {
     return 0;
   }
   return n;
+}
+
+int32_t hb_plan(int64_t nz, int64_t ny, int64_t nx, int32_t itemsize, int64_t halo,
+                double scratch_factor, int64_t usable_bytes, hb_chunk* chunks, int64_t capacity,
+                int64_t* nchunks, int64_t* minimum_bytes) {
+  if (nz < 0 || ny < 0 || nx < 0 || itemsize <= 0 || halo < 0 || !(scratch_factor > 0) ||
+      usable_bytes < 0 || !nchunks) {
+    set_err(nullptr, "hb_plan: bad arguments");
+    return HB_EPARAM;
+  }
+  const double slice_bytes = (double)(ny * nx * (int64_t)itemsize);
+  const double denom = scratch_factor * slice_bytes;
+  // Python's float floor division: the floor of the exact quotient
+  int64_t t = denom > 0 ? (int64_t)std::floor((double)usable_bytes / denom) : INT64_MAX / 4;
+  if (denom > 0) {
+    while ((double)(t + 1) * denom <= (double)usable_bytes) ++t;
+    while (t > 0 && (double)t * denom > (double)usable_bytes) --t;
+  }
+  if (t <= 2 * halo) {
+    const int64_t minimum = (int64_t)std::ceil((double)(2 * halo + 1) * scratch_factor * slice_bytes);
+    if (minimum_bytes) *minimum_bytes = minimum;
+    set_err(nullptr, "budget of " + std::to_string(usable_bytes) + " usable bytes holds only " +
+                         std::to_string(t) + " padded slices but the operator needs more than " +
+                         std::to_string(2 * halo) + "; minimum usable budget is " +
+                         std::to_string(minimum) + " bytes");
+    return HB_EBUDGET_SMALL;
+  }
+  const int64_t n = std::max<int64_t>(t - 2 * halo, 1);
+  const int64_t count = (nz + n - 1) / n;
+  *nchunks = count;
+  if (chunks && capacity >= count) {
+    for (int64_t k = 0; k < count; ++k) {
+      const int64_t z0 = k * n, z1 = std::min(z0 + n, nz);
+      chunks[k] = hb_chunk{z0, z1, std::min(halo, z0), std::min(halo, nz - z1)};
+    }
+  }
+  return HB_OK;
 }
 
 int32_t hb_device_info(int32_t dev, int64_t* free_bytes, int64_t* total_bytes) {

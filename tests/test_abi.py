@@ -88,3 +88,35 @@ def test_session_and_pinned_are_public_api():
 
     assert callable(hb.session) and callable(hb.pinned)
     assert "hb_session_begin" in _native.EXPORTS and "hb_session_end" in _native.EXPORTS
+
+
+def test_hb_plan_matches_plan_chunks(golden):
+    """hb_plan (the C callers' plan_chunks) against the Python planner and the
+    reference's own plans in the golden fixtures (chunking.py:135-174)."""
+    from paper_2511_11890_b200.chunking import MemoryBudget, OpProfile, plan_chunks
+    from paper_2511_11890_b200.errors import BudgetTooSmallError
+
+    L = _native.load()
+    i64 = ctypes.c_int64
+    L.hb_plan.argtypes = [i64, i64, i64, ctypes.c_int32, i64, ctypes.c_double, i64,
+                          ctypes.c_void_p, i64, ctypes.POINTER(i64), ctypes.POINTER(i64)]
+    meta, _ = golden
+    cases = [(p["shape"], p["itemsize"], p["halo"], p["scratch"], p["usable"]) for p in meta["plans"]
+             if "shape" in p]
+    cases += [((100, 1024, 1024), 4, 2, 3, 20 * 2**20), ((37, 5, 7), 2, 3, 8.5, 10**5),
+              ((64, 64, 64), 1, 8, 8, 40 * 64 * 64 * 8 + 3), ((1, 1, 1), 4, 0, 2, 8)]
+    for shape, item, halo, scratch, usable in cases:
+        dt = np.dtype(f"u{item}") if item < 4 else np.dtype(np.float32)
+        n, mn = i64(), i64()
+        buf = (_native.HbChunk * 4096)()
+        rc = L.hb_plan(*shape, item, halo, float(scratch), usable, ctypes.addressof(buf), 4096,
+                       ctypes.byref(n), ctypes.byref(mn))
+        try:
+            plan = plan_chunks(tuple(shape), dt, OpProfile(halo_z=halo, scratch_factor=scratch),
+                               MemoryBudget(usable, 1.0))
+        except BudgetTooSmallError as e:
+            assert rc == 2 and mn.value == e.minimum_bytes  # HB_EBUDGET_SMALL
+            continue
+        assert rc == 0 and n.value == len(plan.chunks)
+        got = [(c.z_start, c.z_stop, c.halo_lo, c.halo_hi) for c in buf[:n.value]]
+        assert got == [(c.z_start, c.z_stop, c.halo_lo, c.halo_hi) for c in plan.chunks]
