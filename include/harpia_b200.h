@@ -18,9 +18,11 @@
  *                     DEVICE-resident block (torch tensors, sharded slabs).
  *   hb_device_info    replaces probe_free_bytes (chunking.py:57-61): free bytes
  *                     come from cudaMemGetInfo instead of psutil.
+ *   hb_plan           restates plan_chunks (chunking.py:135-174) for C callers.
  *   hb_gaussian_weights restates _gaussian_kernel (filters.py:26-30).
- *   hb_se_*           restate StructuringElement.ball/box/cross (morphology.py:49-82)
- *                     as offset lists (used for self-checks; Python builds offsets).
+ *   hb_minmax / hb_histogram, hb_connected_components, hb_label_filter,
+ *   hb_geodesic, hb_edt  replace the global operators' run functions
+ *                     (registry.py:312-417).
  *
  * Status codes map 1:1 onto the reference exception hierarchy (errors.py:4-41);
  * see hb_status.  No torch types cross this boundary: plain pointers and sizes.
