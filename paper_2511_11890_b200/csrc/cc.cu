@@ -109,7 +109,7 @@ __device__ __forceinline__ void cc_union(int* lab, int a, int b) {
 __device__ constexpr int kB26[13][3] = {
     {-1, 0, 0}, {0, -1, 0}, {0, 0, -1}, {-1, 1, 0}, {-1, -1, 0}, {-1, 0, -1}, {-1, 0, 1},
     {0, -1, -1}, {0, -1, 1}, {-1, 1, 1}, {-1, 1, -1}, {-1, -1, 1}, {-1, -1, -1}};
-__host__ __device__ constexpr unsigned b26_adj(int k) {  // neighbours 26-adjacent to k, and k
+__device__ constexpr unsigned b26_adj(int k) {  // neighbours 26-adjacent to k, and k
   unsigned m = 0;
   for (int j = 0; j < 13; ++j) {
     const int a = kB26[k][0] - kB26[j][0], b = kB26[k][1] - kB26[j][1], c = kB26[k][2] - kB26[j][2];
