@@ -367,6 +367,9 @@ std::vector<Range> stage_ranges(const std::vector<StageDesc>& st, int64_t nz, in
 }
 
 // Scratch bytes needed to evaluate the chain (excluding the final output).
+bool widen_eligible(const StageDesc& d, const DevIn& in);
+int64_t widened_nx(int64_t nx, int dt);
+
 size_t chain_scratch(const std::vector<StageDesc>& st, int64_t nz, int64_t ny, int64_t nx,
                      int64_t zo, int64_t nzo) {
   auto rg = stage_ranges(st, nz, zo, nzo);
@@ -381,6 +384,16 @@ size_t chain_scratch(const std::vector<StageDesc>& st, int64_t nz, int64_t ny, i
       int64_t in_n = s == 0 ? nz : (rg[s - 1].b - rg[s - 1].a);
       total += 2 * (size_t)in_n * plane * 4;
     }
+    {  // row-pitch widening (run_stage): widened input + output of the stage
+      StageDesc tmp = st[s];
+      DevIn probe{nullptr, st[s].in_dt, 1, ny, nx};
+      if (widen_eligible(tmp, probe)) {
+        const int64_t nxp = widened_nx(nx, st[s].in_dt);
+        const int64_t in_n = s == 0 ? nz : (rg[s - 1].b - rg[s - 1].a);
+        total += (size_t)(in_n * ny * nxp) * dtype_size(st[s].in_dt) + (size_t)(n * ny * nxp) * 4 + 512;
+        total += (size_t)(n * ny * (nxp - nx)) * 4;  // the stage's own temporaries at the wider pitch
+      }
+    }
     if (st[s].op == HB_OP_LOCAL_THRESHOLD)
       total += local_threshold_scratch(st[s].lt.kind, st[s].in_dt, st[s].lt.w, n, (int64_t)plane) + 256;
     if (st[s].op == HB_OP_LOG || st[s].op == HB_OP_HESSIAN) {
@@ -392,8 +405,8 @@ size_t chain_scratch(const std::vector<StageDesc>& st, int64_t nz, int64_t ny, i
   return total + 4096 * st.size();
 }
 
-cudaError_t run_stage(const StageDesc& d, const DevIn& in, int64_t zo, int64_t nzo, void* out,
-                      PoolAlloc& pa, cudaStream_t s, int64_t* launches) {
+cudaError_t run_stage_impl(const StageDesc& d, const DevIn& in, int64_t zo, int64_t nzo, void* out,
+                           PoolAlloc& pa, cudaStream_t s, int64_t* launches) {
   const size_t plane = (size_t)in.ny * in.nx;
   switch (d.op) {
     case HB_OP_IDENTITY:
@@ -501,6 +514,57 @@ cudaError_t run_stage(const StageDesc& d, const DevIn& in, int64_t zo, int64_t n
 }
 
 // Evaluate the chain on block `in`, writing [zo, zo+nzo) into `out`.
+// Row pitch widening.  The TMA / vector kernels need 16-byte rows; a volume
+// whose x extent is not a multiple of 16 / itemsize would fall to the generic
+// per-pass kernels (10-40x slower).  For the single-window operators (each
+// output depends on its clamped input window only: gaussian, unsharp, mean,
+// erode, dilate) replicating the last column out to the aligned width gives
+// exactly the clamp-to-edge values, so the stage runs on the widened block
+// and its first nx columns are the result, bit for bit.
+template <typename E>
+__global__ void k_widen_rows(const E* __restrict__ src, E* __restrict__ dst, int64_t rows, int nx, int nxp) {
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+    const E* a = src + r * nx;
+    E* b = dst + r * nxp;
+    for (int x = threadIdx.x; x < nxp; x += blockDim.x) b[x] = a[x < nx ? x : nx - 1];
+  }
+}
+
+bool widen_eligible(const StageDesc& d, const DevIn& in) {
+  const bool op = d.op == HB_OP_GAUSSIAN || d.op == HB_OP_UNSHARP || d.op == HB_OP_MEAN ||
+                  d.op == HB_OP_ERODE || d.op == HB_OP_DILATE;
+  const int64_t al = 16 / dtype_size(in.dt);
+  return op && in.nx % al != 0 && in.nx > 1 && !std::getenv("HB_NO_WIDEN");
+}
+
+int64_t widened_nx(int64_t nx, int dt) {
+  const int64_t al = 16 / dtype_size(dt);
+  return (nx + al - 1) / al * al;
+}
+
+cudaError_t run_stage(const StageDesc& d, const DevIn& in, int64_t zo, int64_t nzo, void* out,
+                      PoolAlloc& pa, cudaStream_t s, int64_t* launches) {
+  if (!widen_eligible(d, in)) return run_stage_impl(d, in, zo, nzo, out, pa, s, launches);
+  const int64_t nxp = widened_nx(in.nx, in.dt);
+  const size_t ies = dtype_size(in.dt), oes = dtype_size(d.out_dt);
+  void* wi = pa.get((size_t)(in.nz * in.ny * nxp) * ies);
+  void* wo = pa.get((size_t)(nzo * in.ny * nxp) * oes);
+  if (!wi || !wo) return pa.err;
+  const int64_t rows = in.nz * in.ny;
+  const int g = (int)std::min<int64_t>(rows, (int64_t)kNumSMs * 32);
+  switch (ies) {
+    case 1: k_widen_rows<uint8_t><<<g, 128, 0, s>>>((const uint8_t*)in.p, (uint8_t*)wi, rows, (int)in.nx, (int)nxp); break;
+    case 2: k_widen_rows<uint16_t><<<g, 128, 0, s>>>((const uint16_t*)in.p, (uint16_t*)wi, rows, (int)in.nx, (int)nxp); break;
+    default: k_widen_rows<uint32_t><<<g, 128, 0, s>>>((const uint32_t*)in.p, (uint32_t*)wi, rows, (int)in.nx, (int)nxp); break;
+  }
+  if (launches) *launches += 1;
+  DevIn win{wi, in.dt, in.nz, in.ny, nxp};
+  cudaError_t e = run_stage_impl(d, win, zo, nzo, wo, pa, s, launches);
+  if (e != cudaSuccess) return e;
+  return cudaMemcpy2DAsync(out, (size_t)in.nx * oes, wo, (size_t)nxp * oes, (size_t)in.nx * oes,
+                           (size_t)(nzo * in.ny), cudaMemcpyDeviceToDevice, s);
+}
+
 cudaError_t run_chain(const std::vector<StageDesc>& st, const DevIn& in, int64_t zo,
                       int64_t nzo, void* out, PoolAlloc& pa, cudaStream_t s,
                       int64_t* launches) {
