@@ -387,6 +387,7 @@ size_t chain_scratch(const std::vector<StageDesc>& st, int64_t nz, int64_t ny, i
     {  // row-pitch widening (run_stage): widened input + output of the stage
       StageDesc tmp = st[s];
       DevIn probe{nullptr, st[s].in_dt, 1, ny, nx};
+      if (tmp.op == HB_OP_LOG || tmp.op == HB_OP_HESSIAN) tmp.op = HB_OP_GAUSSIAN;  // their smoothing
       if (widen_eligible(tmp, probe)) {
         const int64_t nxp = widened_nx(nx, st[s].in_dt);
         const int64_t in_n = s == 0 ? nz : (rg[s - 1].b - rg[s - 1].a);
@@ -404,6 +405,9 @@ size_t chain_scratch(const std::vector<StageDesc>& st, int64_t nz, int64_t ny, i
   }
   return total + 4096 * st.size();
 }
+
+cudaError_t run_stage(const StageDesc& d, const DevIn& in, int64_t zo, int64_t nzo, void* out,
+                      PoolAlloc& pa, cudaStream_t s, int64_t* launches);
 
 cudaError_t run_stage_impl(const StageDesc& d, const DevIn& in, int64_t zo, int64_t nzo, void* out,
                            PoolAlloc& pa, cudaStream_t s, int64_t* launches) {
@@ -477,23 +481,14 @@ cudaError_t run_stage_impl(const StageDesc& d, const DevIn& in, int64_t zo, int6
       // smoothed g over [zo-2, zo+nzo+2) ∩ [0, nz) then the cd∘cd stage
       int64_t g0 = std::max<int64_t>(0, zo - 2), g1 = std::min<int64_t>(in.nz, zo + nzo + 2);
       float* g = (float*)pa.get((size_t)(g1 - g0) * plane * 4);
-      float* tmp = (float*)pa.get((size_t)(g1 - g0) * plane * 4);
-      if (!g || !tmp) return pa.err;
-      EpiArgs none;
-      cudaError_t e = cudaSuccess;
-      if (d.precision == HB_PREC_FAST) {
-        e = gaussian_fused(in, g0, g1 - g0, g, d.taps, none, s, launches);
-        if (e == cudaErrorNotSupported) {
-          cudaGetLastError();
-          e = gaussian_generic(in, g0, g1 - g0, g, d.taps, false, none, tmp, s, launches);
-        }
-      } else {
-        e = gaussian_exact_fused(in, g0, g1 - g0, g, d.taps, none, tmp, s, launches);
-        if (e == cudaErrorNotSupported) {
-          cudaGetLastError();
-          e = gaussian_generic(in, g0, g1 - g0, g, d.taps, true, none, tmp, s, launches);
-        }
-      }
+      if (!g) return pa.err;
+      // the smoothing is a plain gaussian stage (same taps and precision), so
+      // ragged rows get the widening of run_stage; g itself stays at nx
+      StageDesc gd = d;
+      gd.op = HB_OP_GAUSSIAN;
+      gd.out_dt = HB_F32;
+      gd.amount = 0.f;
+      cudaError_t e = run_stage(gd, in, g0, g1 - g0, g, pa, s, launches);
       if (e != cudaSuccess) return e;
       if (d.op == HB_OP_HESSIAN) {
         // component index -> (a, b) axes, x = 2, y = 1, z = 0 (filters.py:228-231)
