@@ -652,3 +652,23 @@ def test_connected_components_sharded_single_rank_device(hb, oracle):
     want, n = oracle.connected_components(m, 26)
     got, total = sharding.connected_components_sharded(torch.from_numpy(m).cuda(), 26, 0, 1)
     assert total == n and np.array_equal(got.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("dt,nx", [("u8", 13), ("u16", 21), ("f32", 30), ("u8", 47)])
+def test_row_widening_exact(hb, oracle, dt, nx):
+    """x extents off the 16-byte pitch run the TMA kernels on edge-replicated
+    widened rows (executor run_stage): results stay bit-exact (exact modes,
+    morphology, LoG) / within the float tolerance (fast mean)."""
+    from paper_2511_11890_b200 import filters, morphology
+
+    rng = np.random.default_rng(nx)
+    x = _vol(rng, (19, 23, nx), dt)
+    assert np.array_equal(filters.gaussian(x, 1.5, "exact"), oracle.gaussian(x, 1.5))
+    assert np.array_equal(filters.unsharp(x, 1.0, 1.5, "exact"), oracle.unsharp(x, 1.0, 1.5))
+    assert np.array_equal(filters.log(x, 1.2), oracle.log(x, 1.2))
+    assert float_close(filters.mean(x, 2), oracle.mean(x, 2)) <= FLOAT_TOL
+    for se in ("ball:3", "box:1", "cross:2"):
+        s = morphology.StructuringElement.parse(se)
+        offs = oracle.parse_se(se)
+        assert np.array_equal(morphology.erode(x, s), oracle.erode(x, offs)), se
+        assert np.array_equal(morphology.dilate(x, s), oracle.dilate(x, offs)), se
