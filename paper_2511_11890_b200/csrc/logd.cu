@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(32 * W) k_log_stream(const LogArgs a) {
       xxv[r][1] = sec_fast(l1, v.y, v.w);
       xxv[r][2] = sec_fast(v.x, v.z, r1);
       xxv[r][3] = sec_fast(v.y, v.w, r2);
-      if (x_face) {
+      if (x_face && act) {  // inactive lanes (xl >= nx) would index past the window
         const float xw[8] = {l2, l1, v.x, v.y, v.z, v.w, r1, r2};
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
