@@ -1,15 +1,16 @@
 #!/usr/bin/env python
-"""Benchmark of the B200-native Harpia hot path (BASELINE.json configs[1]).
+"""Benchmark of the B200-native Harpia hot path.
 
-Workload (one "step"): the 3x3x3 median (r=1) AND the 3x3x3 mean (r=1) over a
-1024^3 float32 synthetic volume per GPU — BASELINE.json configs[1]
-("3x3x3 median and 3D mean filter on a 1024^3 float32 volume, chunked with
-halos").  ``value`` = output voxels of both filters per second, whole job
+Workload (one "step"): the two filters the metric names — the 3D Gaussian
+(sigma=2, fast fp32) AND the 3x3x3 median (r=1) — over a 1024^3 float32
+synthetic volume per GPU (BASELINE.json configs[1]'s size and the op pair of
+configs[4]).  ``value`` = output voxels of both filters per second, whole job
 (all ranks), device-resident inputs; ``e2e`` = the same step through the
 public API ``registry.run_operator`` from pinned host memory with a budget
 that forces >= 4 halo'd chunks (host->device and device->host inside the
 timed region).  Multi-GPU: weak scaling, one 1024-slice z-slab per rank, no
-data-path collective (each rank owns its padded range).
+data-path collective (each rank owns its padded range).  ``filters`` adds
+configs[0] (gaussian 256^3, single chunk) and the configs[1] mean.
 
 ``--impl reference`` times the reference algorithm on the host cores instead
 (the CPU restatement in oracle/, all threads; the reference itself is Python
@@ -35,7 +36,7 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "Gvoxel/s per filter (3D Gaussian, median) at 1/2/4/8 B200; % HBM roofline"
 UNIT = "Gvoxel/s"
-BYTES_PER_VOXEL = 8  # f32 in + f32 out (SURVEY.md §8(d), configs C1/C2)
+BYTES_PER_VOXEL = 8  # f32 in + f32 out (SURVEY.md §8(d), configs C1/C2/C5)
 
 
 def parse():
@@ -177,41 +178,62 @@ def max_over_ranks(world, value: float) -> float:
 
 
 # --------------------------------------------------------------------------
-# CPU reference arm / baseline (the oracle restatement, all host threads)
+# CPU reference arm / baseline (the oracle restatement, all host threads).
+# The baseline leg also CHECKS the GPU: it evaluates a slab of the very input
+# the timed region used and compares the GPU's output slices with it.
 # --------------------------------------------------------------------------
-def cpu_sample_run(slices: int, yx: int, seed: int = 0):
+HALO_G = 8  # gaussian sigma=2: ceil(4 sigma)
+
+
+def cpu_sample_run(block: np.ndarray):
+    """Oracle gaussian(sigma=2) + median(r=1) of the S output slices centred in
+    ``block`` (S + 2*HALO_G slices).  Returns (t_gauss, t_median, g, m, S*Y*X)."""
     from oracle import oracle as O
 
-    rng = np.random.default_rng(seed)
-    x = rng.random((slices + 2, yx, yx), dtype=np.float32)  # +1 halo slice each side
+    s_out = block.shape[0] - 2 * HALO_G
     t0 = time.perf_counter()
-    O.median(x, 1)
+    g = O.gaussian(block, 2.0)[HALO_G:HALO_G + s_out]
     t1 = time.perf_counter()
-    O.mean(x, 1)
+    m = O.median(block[HALO_G - 1:HALO_G + s_out + 1], 1)[1:1 + s_out]
     t2 = time.perf_counter()
-    return (t1 - t0), (t2 - t1), slices * yx * yx
+    return (t1 - t0), (t2 - t1), g, m, s_out * block.shape[1] * block.shape[2]
 
 
-def calibrate_cpu(yx: int, target_s: float = 4.0) -> int:
-    tm, tmean, vox = cpu_sample_run(1, yx)
-    per_slice = (tm + tmean) / 1  # seconds per output slice (both filters), upper bound
-    return int(max(1, min(64, target_s / max(per_slice, 1e-6))))
+def calibrate_cpu(yx: int, target_s: float) -> int:
+    rng = np.random.default_rng(0)
+    probe = rng.random((8 + 2 * HALO_G, yx, yx), dtype=np.float32)
+    cpu_sample_run(probe)  # thread-pool spin-up
+    tg, tm, _, _, _ = cpu_sample_run(probe)
+    return int(max(1, min(96, 8 * target_s / max(tg + tm, 1e-6))))
 
 
-def cpu_baseline(args, yx):
+def cpu_baseline_and_parity(x, out_g, out_m, yx):
+    """cpu_baseline (oracle port, all OpenMP threads) on a slab of the timed
+    input; the same slab's oracle output is the parity check of the GPU's."""
     from oracle import oracle as O
 
     slices = calibrate_cpu(yx, target_s=5.0)
-    runs = [cpu_sample_run(slices, yx, seed=s) for s in range(2)]
-    best = min(r[0] + r[1] for r in runs)
-    vox = runs[0][2]
-    return {"value": round(2 * vox / best / 1e9, 6), "unit": UNIT, "cores": O.num_threads(),
-            "kind": "port",
-            "sample": f"median r=1 + mean r=1 on a {slices}x{yx}x{yx} f32 slab (+1 halo slice "
-                      f"each side) of the same U[0,1) workload, oracle/harpia_oracle.c with "
-                      f"{O.num_threads()} OpenMP threads, best of 2",
-            "median_mvox_s": round(vox / min(r[0] for r in runs) / 1e6, 3),
-            "mean_mvox_s": round(vox / min(r[1] for r in runs) / 1e6, 3)}
+    nz = out_g.shape[0]
+    z0 = max(0, nz // 2 - slices // 2)
+    block = x[z0:z0 + slices + 2 * HALO_G].cpu().numpy()  # block slice z0+8 = output z0
+    tg, tm, g, m, vox = cpu_sample_run(block)
+    tg2, tm2, _, _, _ = cpu_sample_run(block)
+    tg, tm = min(tg, tg2), min(tm, tm2)
+    got_g = out_g[z0:z0 + slices].cpu().numpy()
+    got_m = out_m[z0:z0 + slices].cpu().numpy()
+    scale = float(np.max(np.abs(g)))
+    g_err = float(np.max(np.abs(got_g.astype(np.float64) - g)) / scale)
+    parity = {"gaussian_s2_fast": {"max_norm_rel": g_err, "tol": 1e-5, "ok": g_err <= 1e-5},
+              "median_r1": {"bit_exact": bool(np.array_equal(got_m, m))},
+              "sample": f"output slices [{z0}, {z0 + slices}) of the timed {nz}^3 run vs oracle/"}
+    cpu = {"value": round(2 * vox / (tg + tm) / 1e9, 6), "unit": UNIT, "cores": O.num_threads(),
+           "kind": "port",
+           "sample": f"gaussian sigma=2 + median r=1 on {slices} output slices of {yx}^2 f32 "
+                     f"(a {slices + 2 * HALO_G}-slice padded slab of the timed input), "
+                     f"oracle/harpia_oracle.c with {O.num_threads()} OpenMP threads, best of 2",
+           "gaussian_mvox_s": round(vox / tg / 1e6, 3),
+           "median_mvox_s": round(vox / tm / 1e6, 3)}
+    return cpu, parity
 
 
 def run_reference(args):
@@ -222,26 +244,27 @@ def run_reference(args):
 
     yx = args.size
     slices = calibrate_cpu(yx, target_s=3.0)
+    rng = np.random.default_rng(0)
     for _ in range(args.warmup):
-        cpu_sample_run(slices, yx)
-    times = []
-    vox = 0
+        cpu_sample_run(rng.random((slices + 2 * HALO_G, yx, yx), dtype=np.float32))
+    total, vox = 0.0, 0
     for k in range(args.steps):
-        tm, tmean, vox = cpu_sample_run(slices, yx, seed=k)
-        times.append(tm + tmean)
-    total = sum(times)
+        block = np.random.default_rng(k).random((slices + 2 * HALO_G, yx, yx), dtype=np.float32)
+        tg, tm, _, _, vox = cpu_sample_run(block)
+        total += tg + tm
     value = 2 * vox * args.steps / total / 1e9
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(1e3 * total / args.steps, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"median r=1 + mean r=1, {yx}^3 f32 (BASELINE configs[1]), "
-                               f"bounded CPU sample of {slices} slices per step",
-                   "global_batch": 1, "seq_len": yx},
+        "config": {"workload": f"gaussian sigma=2 + median r=1, {yx}^3 f32 (BASELINE configs[1] "
+                               f"size; the metric's two filters), bounded CPU sample of {slices} "
+                               f"output slices per step", "global_batch": 1, "seq_len": yx},
         "cpu_baseline": {"value": round(value, 6), "unit": UNIT, "cores": O.num_threads(),
                          "kind": "port",
-                         "sample": f"{slices}x{yx}x{yx} f32 slab per step (+1 halo slice each side)"},
+                         "sample": f"{slices} output slices of {yx}^2 f32 per step "
+                                   f"({slices + 2 * HALO_G}-slice padded slab)"},
         "e2e": {"value": round(value, 6), "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -252,6 +275,9 @@ def run_reference(args):
 # --------------------------------------------------------------------------
 # GPU arm
 # --------------------------------------------------------------------------
+KERNEL_NAMES = {"gaussian": "k_gauss_p2<8,float>", "median": "k_median3_plane<float>"}
+
+
 def run_ours(args):
     import torch
 
@@ -263,35 +289,32 @@ def run_ours(args):
     shape = (n, n, n)
     vox = n * n * n
     gen = torch.Generator(device="cuda").manual_seed(1000 + rank)
-    # padded block: 1 halo slice each side (radius 1); inputs >> L2 (4 GiB vs 126 MB)
-    x = torch.rand((n + 2, n, n), generator=gen, device="cuda", dtype=torch.float32)
-    out_med = torch.empty(shape, device="cuda", dtype=torch.float32)
-    out_mean = torch.empty(shape, device="cuda", dtype=torch.float32)
-    p_med = filters.median_program(1)
-    p_mean = filters.mean_program(1)
+    # one padded block (HALO_G slices each side) feeds both filters: the
+    # gaussian reads +-8 slices, the median +-1 around the same n outputs.
+    # Inputs (4 GiB) >> L2 (126 MB): no flush needed between steps.
+    x = torch.rand((n + 2 * HALO_G, n, n), generator=gen, device="cuda", dtype=torch.float32)
+    out_g = torch.empty(shape, device="cuda", dtype=torch.float32)
+    out_m = torch.empty(shape, device="cuda", dtype=torch.float32)
+    p_g = filters.gaussian_program(2.0, "fast")
+    p_m = filters.median_program(1)
     stream = torch.cuda.current_stream()
 
-    launches = [0]
-
-    def step():
-        launches[0] += _native.apply_device(x, out_med, p_med, 1, stream)
-        launches[0] += _native.apply_device(x, out_mean, p_mean, 1, stream)
-
     for _ in range(args.warmup):
-        step()
+        _native.apply_device(x, out_g, p_g, HALO_G, stream)
+        _native.apply_device(x, out_m, p_m, HALO_G, stream)
     torch.cuda.synchronize()
     barrier(world)
     torch.cuda.synchronize()
-    launches[0] = 0
+    launches = 0
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with Clocks(local) as clk:
         start.record(stream)
         for k in range(args.steps):
             ev[k][0].record(stream)
-            launches[0] += _native.apply_device(x, out_med, p_med, 1, stream)
+            launches += _native.apply_device(x, out_g, p_g, HALO_G, stream)
             ev[k][1].record(stream)
-            launches[0] += _native.apply_device(x, out_mean, p_mean, 1, stream)
+            launches += _native.apply_device(x, out_m, p_m, HALO_G, stream)
             ev[k][2].record(stream)
         end.record(stream)
         torch.cuda.synchronize()
@@ -299,30 +322,38 @@ def run_ours(args):
     torch.cuda.synchronize()
     ms_local = start.elapsed_time(end)
     ms = max_over_ranks(world, ms_local)
-    med_ms = statistics.mean(e[0].elapsed_time(e[1]) for e in ev)
-    mean_ms = statistics.mean(e[1].elapsed_time(e[2]) for e in ev)
+    g_ms = statistics.mean(e[0].elapsed_time(e[1]) for e in ev)
+    m_ms = statistics.mean(e[1].elapsed_time(e[2]) for e in ev)
     value = world * 2 * vox * args.steps / (ms * 1e-3) / 1e9
-    gpu_launches = launches[0]
+    gpu_launches = launches
     clocks = clk.summary()
     peak, peak_kind = peaks()
-    dominant = "median" if med_ms >= mean_ms else "mean"
-    dom_ms = max(med_ms, mean_ms)
+    dominant = "median" if m_ms >= g_ms else "gaussian"
+    dom_ms = max(m_ms, g_ms)
     achieved = BYTES_PER_VOXEL * vox / (dom_ms * 1e-3) / 1e9
     tr = traffic_from_profiles().get(dominant)
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": tr,
-                "kernel": f"{dominant} r=1 ({'k_median3_plane' if dominant == 'median' else 'k_box_stream<float,1>'})",
-                "peak_kind": peak_kind,
-                "algorithmic_bytes_per_launch": BYTES_PER_VOXEL * vox}
-    filters_out = {
-        "median_r1": {"gvox_s": round(vox / (med_ms * 1e-3) / 1e9, 3), "ms": round(med_ms, 3),
-                      "hbm_frac": round(BYTES_PER_VOXEL * vox / (med_ms * 1e-3) / 1e9 / peak, 4)},
-        "mean_r1": {"gvox_s": round(vox / (mean_ms * 1e-3) / 1e9, 3), "ms": round(mean_ms, 3),
-                    "hbm_frac": round(BYTES_PER_VOXEL * vox / (mean_ms * 1e-3) / 1e9 / peak, 4)},
-    }
-    del x, out_med, out_mean
-    torch.cuda.synchronize()
+                "kernel": f"{dominant} ({KERNEL_NAMES[dominant]})", "peak_kind": peak_kind,
+                "algorithmic_bytes_per_launch": BYTES_PER_VOXEL * vox,
+                "launch_ms": round(dom_ms, 4)}
 
+    def frac(ms_, nbytes=BYTES_PER_VOXEL * vox):
+        return round(nbytes / (ms_ * 1e-3) / 1e9 / peak, 4)
+
+    filters_out = {
+        f"gaussian_s2_{n}": {"gvox_s": round(vox / (g_ms * 1e-3) / 1e9, 3), "ms": round(g_ms, 4),
+                             "hbm_frac": frac(g_ms), "kernel": KERNEL_NAMES["gaussian"]},
+        f"median_r1_{n}": {"gvox_s": round(vox / (m_ms * 1e-3) / 1e9, 3), "ms": round(m_ms, 4),
+                           "hbm_frac": frac(m_ms), "kernel": KERNEL_NAMES["median"]},
+    }
+
+    cpu = parity = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu, parity = cpu_baseline_and_parity(x, out_g, out_m, n)
+    del x, out_g, out_m
+    torch.cuda.synchronize()
+    filters_out.update(side_filters(n, peak, stream))
     if args.extra:
         filters_out.update(extra_breakdown(n, peak))
 
@@ -334,15 +365,19 @@ def run_ours(args):
         xin = host_in.numpy()
         o1 = torch.empty(shape, dtype=torch.float32, pin_memory=True).numpy()
         o2 = torch.empty(shape, dtype=torch.float32, pin_memory=True).numpy()
-        op = registry.get_operator("median")
-        prof = op.profile({"radius": 1})
-        t = n // 4 + 2 * prof.halo_z
-        budget = MemoryBudget(int(t * prof.scratch_factor * n * n * 4) + 1, 1.0)
+
+        def budget_of(name, params):
+            prof = registry.get_operator(name).profile(params)
+            t = n // 4 + 2 * prof.halo_z  # >= 4 halo'd chunks
+            return MemoryBudget(int(t * prof.scratch_factor * n * n * 4) + 1, 1.0)
+
+        b_g = budget_of("gaussian", {"sigma": 2.0})
+        b_m = budget_of("median", {"radius": 1})
         reps = []
 
         def e2e_step():
-            _, r1 = registry.run_operator(xin, "median", {"radius": 1}, budget, out=o1)
-            _, r2 = registry.run_operator(xin, "mean", {"radius": 1}, budget, out=o2)
+            _, r1 = registry.run_operator(xin, "gaussian", {"sigma": 2.0}, b_g, out=o1)
+            _, r2 = registry.run_operator(xin, "median", {"radius": 1}, b_m, out=o2)
             return r1, r2
 
         # one device-arena session around the job series: each job still frees
@@ -364,15 +399,11 @@ def run_ours(args):
         e2e = {"value": round(world * 2 * vox * e2e_steps / t_e2e / 1e9, 4), "unit": UNIT,
                "h2d_bytes_per_step": int(r1.h2d_bytes + r2.h2d_bytes),
                "d2h_bytes_per_step": int(r1.d2h_bytes + r2.d2h_bytes),
-               "chunks_per_op": r1.chunk_count, "steps": e2e_steps,
+               "chunks_per_op": [r1.chunk_count, r2.chunk_count], "steps": e2e_steps,
                "device_residual_bytes": int(r1.device_residual_bytes + r2.device_residual_bytes),
-               "path": "registry.run_operator -> hb_run (pinned in/out, 4+ chunks, halos), "
-                       "inside one device-arena session"}
+               "path": "registry.run_operator('gaussian', sigma=2) + ('median', r=1) -> hb_run "
+                       "(pinned in/out, 4+ chunks, halos), inside one device-arena session"}
         gpu_launches += sum(a.kernel_launches + b.kernel_launches for a, b in reps)
-
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_baseline(args, n)
 
     if rank == 0:
         line = {
@@ -380,12 +411,13 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (torch.rand U[0,1) f32, seed 1000+rank)",
-            "config": {"workload": f"median r=1 + mean r=1 on {n}^3 float32 per GPU "
-                                   f"(BASELINE configs[1]); value = output voxels of both filters/s",
+            "config": {"workload": f"gaussian sigma=2 (fast fp32) + median r=1 on {n}^3 float32 "
+                                   f"per GPU (the metric's two filters at BASELINE configs[1]/[4] "
+                                   f"per-GPU size); value = output voxels of both filters/s",
                        "global_batch": world, "seq_len": n,
                        "parallelism": f"z-slab x{world} (weak, no collective)",
                        "l2": "inputs (4 GiB) larger than L2 (126 MB); no flush needed"},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roofline, "cpu_baseline": cpu, "parity": parity, "e2e": e2e,
             "gpu_launches": gpu_launches, "clocks": clocks, "filters": filters_out,
         }
         print(json.dumps(line), flush=True)
@@ -394,6 +426,61 @@ def run_ours(args):
 
         dist.destroy_process_group()
     return 0
+
+
+def _timeit(fn, stream, reps=5):
+    """device time per call: CUDA events on the launching stream, after a warm call."""
+    import torch
+
+    fn()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(reps):
+        fn()
+    b.record(stream)
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps
+
+
+def side_filters(n, peak, stream):
+    """configs[0] (gaussian sigma=2 on 256^3, single chunk) and the configs[1]
+    mean r=1 on n^3, device-resident — reported beside the headline."""
+    import torch
+
+    from paper_2511_11890_b200 import _native, filters
+
+    res = {}
+    e = 256
+    x = torch.rand((e + 2 * HALO_G, e, e), device="cuda")
+    o = torch.empty((e, e, e), device="cuda")
+    prog = filters.gaussian_program(2.0, "fast")
+    # 64 MiB in + 64 MiB out fit in L2 (126 MB) only partly; flush between
+    # launches so every timed launch reads from HBM
+    flush = torch.empty(256 * 2 ** 20 // 4, device="cuda")
+    ms_tot, reps = 0.0, 10
+    for i in range(reps + 1):
+        flush.fill_(1.0)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        _native.apply_device(x, o, prog, HALO_G, stream)
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms_tot += a.elapsed_time(b) if i else 0.0  # launch 0 warms up
+    ms = ms_tot / reps
+    res["gaussian_s2_256_c0"] = {"gvox_s": round(e ** 3 / ms / 1e6, 3), "ms": round(ms, 4),
+                                 "hbm_frac": round(8 * e ** 3 / ms / 1e6 / peak, 4),
+                                 "l2": "flushed (256 MiB write) before every launch"}
+    del x, o, flush
+    x = torch.rand((n + 2, n, n), device="cuda")
+    o = torch.empty((n, n, n), device="cuda")
+    prog = filters.mean_program(1)
+    ms = _timeit(lambda: _native.apply_device(x, o, prog, 1, stream), stream)
+    res[f"mean_r1_{n}"] = {"gvox_s": round(n ** 3 / ms / 1e6, 3), "ms": round(ms, 4),
+                           "hbm_frac": round(8 * n ** 3 / ms / 1e6 / peak, 4)}
+    del x, o
+    torch.cuda.synchronize()
+    return res
 
 
 def extra_breakdown(n, peak):
@@ -405,27 +492,16 @@ def extra_breakdown(n, peak):
     res = {}
     stream = torch.cuda.current_stream()
 
-    def timeit(fn, reps=5):  # device time per call, CUDA events on the launch stream
-        fn()
-        torch.cuda.synchronize()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        for _ in range(reps):
-            fn()
-        b.record(stream)
-        torch.cuda.synchronize()
-        return a.elapsed_time(b) / reps
+    def timeit(fn, reps=5):
+        return _timeit(fn, stream, reps)
 
-    for edge, sigma in ((256, 2.0), (n, 2.0)):
-        x = torch.rand((edge + 16, edge, edge), device="cuda")
-        o = torch.empty((edge, edge, edge), device="cuda")
-        for prec in ("fast", "exact"):
-            prog = filters.gaussian_program(sigma, prec)
-            ms = timeit(lambda: _native.apply_device(x, o, prog, 8, stream))
-            v = edge ** 3
-            res[f"gaussian_s2_{edge}_{prec}"] = {"gvox_s": round(v / ms / 1e6, 3), "ms": round(ms, 3),
-                                                 "hbm_frac": round(8 * v / ms / 1e6 / peak, 4)}
-        del x, o
+    x = torch.rand((n + 16, n, n), device="cuda")
+    o = torch.empty((n, n, n), device="cuda")
+    prog = filters.gaussian_program(2.0, "exact")
+    ms = timeit(lambda: _native.apply_device(x, o, prog, 8, stream))
+    res[f"gaussian_s2_{n}_exact"] = {"gvox_s": round(n ** 3 / ms / 1e6, 3), "ms": round(ms, 3),
+                                     "hbm_frac": round(8 * n ** 3 / ms / 1e6 / peak, 4)}
+    del x, o
     # configs[2]: grey (u16) and binary (u8) erosion + dilation, ball:3, 2048^3
     big = 2048
     ball = morphology.StructuringElement.ball(3)

@@ -391,8 +391,11 @@ size_t chain_scratch(const std::vector<StageDesc>& st, int64_t nz, int64_t ny, i
       if (widen_eligible(tmp, probe)) {
         const int64_t nxp = widened_nx(nx, st[s].in_dt);
         const int64_t in_n = s == 0 ? nz : (rg[s - 1].b - rg[s - 1].a);
-        total += (size_t)(in_n * ny * nxp) * dtype_size(st[s].in_dt) + (size_t)(n * ny * nxp) * 4 + 512;
-        total += (size_t)(n * ny * (nxp - nx)) * 4;  // the stage's own temporaries at the wider pitch
+        // LoG / hessian widen their smoothing, which produces up to n + 4 slices
+        const bool smooth = st[s].op == HB_OP_LOG || st[s].op == HB_OP_HESSIAN;
+        const int64_t wn = smooth ? std::min<int64_t>(in_n, (int64_t)n + 4) : (int64_t)n;
+        total += (size_t)(in_n * ny * nxp) * dtype_size(st[s].in_dt) + (size_t)(wn * ny * nxp) * 4 + 512;
+        total += (size_t)(wn * ny * nxp) * 4;  // the stage's own temporaries at the wider pitch
       }
     }
     if (st[s].op == HB_OP_LOCAL_THRESHOLD)
@@ -542,19 +545,36 @@ cudaError_t run_stage(const StageDesc& d, const DevIn& in, int64_t zo, int64_t n
   if (!widen_eligible(d, in)) return run_stage_impl(d, in, zo, nzo, out, pa, s, launches);
   const int64_t nxp = widened_nx(in.nx, in.dt);
   const size_t ies = dtype_size(in.dt), oes = dtype_size(d.out_dt);
-  void* wi = pa.get((size_t)(in.nz * in.ny * nxp) * ies);
-  void* wo = pa.get((size_t)(nzo * in.ny * nxp) * oes);
-  if (!wi || !wo) return pa.err;
-  const int64_t rows = in.nz * in.ny;
+  // widen only the slices the stage reads: [zo - halo, zo + nzo + halo) clipped
+  // to the block (faces inside the block are never reached by a clamp, so the
+  // sub-block evaluates exactly as the whole block does)
+  const int64_t za = std::max<int64_t>(0, zo - d.halo);
+  const int64_t zb = std::min<int64_t>(in.nz, zo + nzo + d.halo);
+  void* wi = pa.get((size_t)((zb - za) * in.ny * nxp) * ies);
+  void* wo = wi ? pa.get((size_t)(nzo * in.ny * nxp) * oes) : nullptr;
+  if (!wi || !wo) {
+    // no room for the widened copies (e.g. hb_apply_device on a device-resident
+    // volume without a budget): the generic kernels run on the block as is
+    if (wi) {
+      cudaFreeAsync(wi, s);
+      pa.ptrs.pop_back();
+    }
+    pa.err = cudaSuccess;
+    cudaGetLastError();
+    return run_stage_impl(d, in, zo, nzo, out, pa, s, launches);
+  }
+  const int64_t rows = (zb - za) * in.ny;
+  const size_t off = (size_t)(za * in.ny * in.nx) * ies;
+  const void* src = static_cast<const char*>(in.p) + off;
   const int g = (int)std::min<int64_t>(rows, (int64_t)kNumSMs * 32);
   switch (ies) {
-    case 1: k_widen_rows<uint8_t><<<g, 128, 0, s>>>((const uint8_t*)in.p, (uint8_t*)wi, rows, (int)in.nx, (int)nxp); break;
-    case 2: k_widen_rows<uint16_t><<<g, 128, 0, s>>>((const uint16_t*)in.p, (uint16_t*)wi, rows, (int)in.nx, (int)nxp); break;
-    default: k_widen_rows<uint32_t><<<g, 128, 0, s>>>((const uint32_t*)in.p, (uint32_t*)wi, rows, (int)in.nx, (int)nxp); break;
+    case 1: k_widen_rows<uint8_t><<<g, 128, 0, s>>>((const uint8_t*)src, (uint8_t*)wi, rows, (int)in.nx, (int)nxp); break;
+    case 2: k_widen_rows<uint16_t><<<g, 128, 0, s>>>((const uint16_t*)src, (uint16_t*)wi, rows, (int)in.nx, (int)nxp); break;
+    default: k_widen_rows<uint32_t><<<g, 128, 0, s>>>((const uint32_t*)src, (uint32_t*)wi, rows, (int)in.nx, (int)nxp); break;
   }
   if (launches) *launches += 1;
-  DevIn win{wi, in.dt, in.nz, in.ny, nxp};
-  cudaError_t e = run_stage_impl(d, win, zo, nzo, wo, pa, s, launches);
+  DevIn win{wi, in.dt, zb - za, in.ny, nxp};
+  cudaError_t e = run_stage_impl(d, win, zo - za, nzo, wo, pa, s, launches);
   if (e != cudaSuccess) return e;
   return cudaMemcpy2DAsync(out, (size_t)in.nx * oes, wo, (size_t)nxp * oes, (size_t)in.nx * oes,
                            (size_t)(nzo * in.ny), cudaMemcpyDeviceToDevice, s);
@@ -941,9 +961,9 @@ int32_t hb_plan(int64_t nz, int64_t ny, int64_t nx, int32_t itemsize, int64_t ha
   const double denom = scratch_factor * slice_bytes;
   // Python's float floor division: the floor of the exact quotient
   int64_t t = denom > 0 ? (int64_t)std::floor((double)usable_bytes / denom) : INT64_MAX / 4;
-  if (denom > 0) {
-    while ((double)(t + 1) * denom <= (double)usable_bytes) ++t;
-    while (t > 0 && (double)t * denom > (double)usable_bytes) --t;
+  if (denom > 0) {  // the quotient is within one step of the floor; bounded fix-ups
+    for (int i = 0; i < 4 && (double)(t + 1) * denom <= (double)usable_bytes; ++i) ++t;
+    for (int i = 0; i < 4 && t > 0 && (double)t * denom > (double)usable_bytes; ++i) --t;
   }
   if (t <= 2 * halo) {
     const int64_t minimum = (int64_t)std::ceil((double)(2 * halo + 1) * scratch_factor * slice_bytes);

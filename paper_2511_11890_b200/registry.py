@@ -85,11 +85,31 @@ def validate_params(op: Operator, raw: dict) -> dict:
     return params
 
 
+def _unvalidated(op: Operator, raw: dict) -> dict:
+    """``validate=False`` (the service's job path, service.py:131-139): take
+    the caller's values as given, but fill the schema defaults the reference
+    schema does not have (e.g. ``precision``) so the profile/program see them."""
+    params = {k: d for k, (_c, d) in op.schema.items() if d is not REQUIRED and k not in raw}
+    params.update(raw)
+    return params
+
+
 def _program_for(op: Operator, params: dict) -> _native.DeviceProgram:
     try:
         return op.program(params)
     except ParameterError:
         raise
+    except KeyError as exc:  # unvalidated params missing a required key
+        raise ParameterError(f"{op.name}: missing required parameter {exc.args[0]!r}") from exc
+    except (TypeError, ValueError) as exc:
+        raise ParameterError(f"{op.name}: bad parameters: {exc}") from exc
+
+
+def _profile_for(op: Operator, params: dict) -> OpProfile:
+    try:
+        return op.profile(params)
+    except KeyError as exc:
+        raise ParameterError(f"{op.name}: missing required parameter {exc.args[0]!r}") from exc
 
 
 def run_operator(
@@ -106,14 +126,14 @@ def run_operator(
     profile against ``budget`` (default: 80% of free device memory) and stream
     the volume through the operator's device program chunk by chunk."""
     op = get_operator(name)
-    params = validate_params(op, params or {}) if validate else dict(params or {})
+    params = validate_params(op, params or {}) if validate else _unvalidated(op, params or {})
     if budget is None:
         budget = profile_budget()
     if op.kind == "global":  # registry.py:99-103: global operators run themselves
         return op.run(data, params, budget, cancel)
     program = _program_for(op, params)
     arr, restore = filters.coerce_input(data, program)
-    out, report = execute_chunked(arr, program, op.profile(params), budget, params,
+    out, report = execute_chunked(arr, program, _profile_for(op, params), budget, params,
                                   aux=aux, cancel=cancel, **exec_kw)
     return (restore(out) if restore else out), report
 
