@@ -49,6 +49,11 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--extra", action="store_true", help="also time gaussian/erode breakdown")
+    ap.add_argument("--workload", choices=["all", "headline", "sharded", "oocore"], default="all",
+                    help="all = headline line + the configs[3] sharded and configs[4] "
+                         "out-of-core workloads in its 'workloads' object")
+    ap.add_argument("--sharded-size", type=int, default=2048)
+    ap.add_argument("--oocore-size", type=int, default=4096)
     return ap.parse_args()
 
 
@@ -405,6 +410,18 @@ def run_ours(args):
                        "(pinned in/out, 4+ chunks, halos), inside one device-arena session"}
         gpu_launches += sum(a.kernel_launches + b.kernel_launches for a, b in reps)
 
+    workloads = None
+    if args.workload == "all":
+        workloads = {}
+        for name, fn in (("c3_sharded_unsharp_log", workload_sharded),
+                         ("c5_oocore_gauss_median", workload_oocore)):
+            try:
+                workloads[name] = fn(args, world, rank, local)
+            except Exception as exc:  # reported, never silently dropped
+                workloads[name] = {"error": f"{type(exc).__name__}: {exc}"[:400]}
+            torch.cuda.synchronize()
+            barrier(world)
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world,
@@ -419,6 +436,7 @@ def run_ours(args):
                        "l2": "inputs (4 GiB) larger than L2 (126 MB); no flush needed"},
             "roofline": roofline, "cpu_baseline": cpu, "parity": parity, "e2e": e2e,
             "gpu_launches": gpu_launches, "clocks": clocks, "filters": filters_out,
+            "workloads": workloads,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -535,10 +553,210 @@ def extra_breakdown(n, peak):
     return res
 
 
+# --------------------------------------------------------------------------
+# Scale workloads (the multi-GPU rows of BASELINE.json), run inside the
+# default bench line at every N so a scaling run measures them too.
+# --------------------------------------------------------------------------
+GEN_BLOCK = 8  # input generated in 8-slice blocks seeded by global block index
+
+
+def gen_slices(z0, z1, ny, nx, out, seed_base):
+    """Deterministic synthetic U[0,1) f32 slices [z0, z1) of a global volume
+    (any rank can regenerate any slice) into the device tensor ``out``."""
+    import torch
+
+    b0, b1 = z0 // GEN_BLOCK, (z1 + GEN_BLOCK - 1) // GEN_BLOCK
+    for b in range(b0, b1):
+        g = torch.Generator(device=out.device).manual_seed(seed_base + b)
+        blk = torch.rand((GEN_BLOCK, ny, nx), generator=g, device=out.device)
+        a, e = max(z0, b * GEN_BLOCK), min(z1, (b + 1) * GEN_BLOCK)
+        out[a - z0:e - z0].copy_(blk[a - b * GEN_BLOCK:e - b * GEN_BLOCK])
+        del blk
+
+
+def _ev_ms(fn, reps, warm, world, stream):
+    import torch
+
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    barrier(world)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(reps):
+        fn()
+    b.record(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    return max_over_ranks(world, a.elapsed_time(b)) / reps
+
+
+def workload_sharded(args, world, rank, local):
+    """BASELINE configs[3]: unsharp(sigma=1, a=1.5) -> LoG(sigma=2) on a
+    2048^3 f32 volume z-slab sharded over the N ranks (strong scaling: the
+    volume is fixed), one NCCL neighbour exchange per chained stage with the
+    interior computed while the halos are in flight (sharding.run_sharded).
+    Inputs live in library-pool device buffers; value = 2048^3 / step time."""
+    import torch
+
+    from paper_2511_11890_b200 import _native, filters, sharding
+
+    n = args.sharded_size
+    slab = sharding.partition(n, world)[rank]
+    prog = filters.chain(filters.unsharp_program(1.0, 1.5), filters.log_program(2.0))
+    halos = [st.halo() for st in prog.stages]
+    stream = torch.cuda.current_stream()
+    with _native.session():
+        src = sharding.alloc_padded(slab.size, (n, n), torch.float32, torch.empty(0, device="cuda"),
+                                    halos[0] if rank > 0 else 0, halos[0] if rank < world - 1 else 0)
+        gen_slices(slab.z0, slab.z1, n, n, src.interior, 5000)
+        res = {}
+
+        def step():
+            res["out"] = sharding.run_sharded(src, prog, rank, world)
+
+        steps = max(1, min(args.steps, 5))
+        ms = _ev_ms(step, steps, max(1, min(args.warmup, 2)), world, stream)
+        out = res.pop("out")
+        # exchange alone (the LoG stage's 10-slice faces), to show what the
+        # interior-first schedule hides
+        xch_ms = None
+        if world > 1:
+            tr = sharding.DistTransport(rank, world)
+            xch_ms = _ev_ms(lambda: tr.finish(tr.start(src, halos[1])), 3, 1, world, stream)
+        parity = None
+        if rank == 0 and not args.no_cpu:
+            parity = _sharded_parity(out, slab, n, halos, world)
+        del out, src
+        torch.cuda.synchronize()
+    face = halos[1] * n * n * 4
+    return {"workload": f"configs[3]: unsharp(1, 1.5) -> LoG(2) on {n}^3 f32, z-slab x{world}, "
+                        "NCCL halo exchange per stage, interior-first overlap",
+            "value": round(n ** 3 / (ms * 1e-3) / 1e9, 3), "unit": UNIT, "scaling": "strong",
+            "ms_per_step": round(ms, 3), "n_gpus": world, "steps": steps,
+            "exchange_only_ms": None if xch_ms is None else round(xch_ms, 3),
+            "exchange_bytes_per_face": {"unsharp": halos[0] * n * n * 4, "log": face},
+            "slab_slices": slab.size, "parity": parity,
+            "buffers": "library pool (hb_device_alloc), trimmed at session end"}
+
+
+def _sharded_parity(out, slab, n, halos, world):
+    """rank 0's first output slice and its last one (which, at N > 1, depends
+    on the neighbour's ghost slices) against the oracle chain on a padded slab
+    regenerated from the deterministic generator."""
+    import torch
+
+    from oracle import oracle as O
+
+    H = sum(halos)
+    res = {}
+    for z in sorted({slab.z0, slab.z1 - 1}):
+        a, b = max(0, z - H), min(n, z + H + 1)
+        blk = torch.empty((b - a, n, n), device="cuda")
+        gen_slices(a, b, n, n, blk, 5000)
+        xh = blk.cpu().numpy()
+        ref = O.log(O.unsharp(xh, 1.0, 1.5), 2.0)[z - a]
+        got = out[z - slab.z0].cpu().numpy()
+        err = float(np.max(np.abs(got.astype(np.float64) - ref)) / np.max(np.abs(ref)))
+        res[f"slice_{z}"] = {"max_norm_rel": err, "ok": err <= 1e-5}
+        del blk
+    return res
+
+
+def workload_oocore(args, world, rank, local):
+    """BASELINE configs[4]: Gaussian(2) -> median(1) over a 4096^3 f32 volume
+    that does not fit one GPU, streamed from pinned host memory.  Each rank
+    owns 512 slices (its z-range of the 4096^3 volume plus 9 halo slices each
+    side from host memory) and streams them through ONE fused per-chunk
+    pipeline (registry.run_pipeline -> hb_run: pinned H2D, kernels, D2H,
+    3 streams) on its own PCIe link; weak scaling, 8 ranks = the full volume.
+    value = Gvox/s of all ranks (host-to-host, the e2e of this config)."""
+    import torch
+
+    from paper_2511_11890_b200 import _native, registry
+    from paper_2511_11890_b200.chunking import MemoryBudget
+
+    n = args.oocore_size
+    per = n // 8  # one eighth of the volume per rank (the 8-GPU share)
+    z0 = rank * per
+    halo = 9
+    a, b = max(0, z0 - halo), min(n, z0 + per + halo)
+    need = 2 * (b - a) * n * n * 4
+    try:
+        avail = os.sysconf("SC_AVPHYS_PAGES") * os.sysconf("SC_PAGE_SIZE")
+    except (ValueError, OSError):
+        avail = need * 4
+    if avail < need * max(1, int(os.environ.get("LOCAL_WORLD_SIZE", world))) * 1.15:
+        raise MemoryError(f"host RAM {avail >> 30} GiB free < pinned buffers "
+                          f"{need >> 30} GiB per rank")
+    host_in = torch.empty((b - a, n, n), dtype=torch.float32, pin_memory=True)
+    dev = torch.empty((GEN_BLOCK * 8, n, n), device="cuda")
+    for c0 in range(a, b, dev.shape[0]):  # generate on the GPU, download slab-wise
+        c1 = min(b, c0 + dev.shape[0])
+        gen_slices(c0, c1, n, n, dev[:c1 - c0], 9000)
+        host_in[c0 - a:c1 - a].copy_(dev[:c1 - c0])
+    del dev
+    torch.cuda.synchronize()
+    host_out = torch.empty((b - a, n, n), dtype=torch.float32, pin_memory=True)
+    xin, xout = host_in.numpy(), host_out.numpy()
+    steps_def = [("gaussian", {"sigma": 2.0}), ("median", {"radius": 1})]
+    # budget of a 64 GiB device share (3 chunks at this size, as the 8-GPU job plans)
+    budget = MemoryBudget(int((per // 3 + 2 * halo) * 8 * n * n * 4) + 1, 1.0)
+    with _native.session():
+        t_run = []
+        reps = []
+        for k in range(1 + max(1, min(args.steps, 2))):
+            barrier(world)
+            t0 = time.perf_counter()
+            _, rep = registry.run_pipeline(xin, steps_def, budget, out=xout)
+            t_run.append(time.perf_counter() - t0)
+            reps.append(rep)
+        barrier(world)
+    t = max_over_ranks(world, statistics.median(t_run[1:]))
+    rep = reps[-1]
+    parity = None
+    if rank == 0 and not args.no_cpu:
+        from oracle import oracle as O
+
+        zs = (z0, z0 + per // 2, z0 + per - 1)
+        worst = 0.0
+        for z in zs:
+            lo, hi = max(a, z - halo), min(b, z + halo + 1)
+            ref = O.median(O.gaussian(xin[lo - a:hi - a], 2.0), 1)[z - lo]
+            got = xout[z - a]
+            worst = max(worst, float(np.max(np.abs(got.astype(np.float64) - ref)) / np.max(np.abs(ref))))
+        parity = {"max_norm_rel": worst, "ok": worst <= 1e-5, "slices": list(zs)}
+    vox = per * n * n
+    res = {"workload": f"configs[4]: gaussian(2) -> median(1) out-of-core over {n}^3 f32, "
+                       f"{per} slices per rank (+{halo}-slice halos from host), pinned host "
+                       f"memory, hb_run 3-stream pipeline; x{world} ranks",
+           "value": round(world * vox / t / 1e9, 3), "unit": UNIT, "scaling": "weak",
+           "s_per_step": round(t, 4), "n_gpus": world,
+           "pcie_gb_s_each_way_per_rank": round(rep.h2d_bytes / t / 1e9, 2),
+           "h2d_bytes_per_rank": int(rep.h2d_bytes), "d2h_bytes_per_rank": int(rep.d2h_bytes),
+           "chunks": rep.chunk_count, "device_peak_bytes": int(rep.device_peak_bytes),
+           "device_residual_bytes": int(rep.device_residual_bytes),
+           "kernel_s": round(rep.kernel_seconds, 4), "parity": parity}
+    del host_in, host_out
+    return res
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.workload in ("sharded", "oocore"):
+        world, rank, local = dist_setup(args)
+        fn = workload_sharded if args.workload == "sharded" else workload_oocore
+        res = fn(args, world, rank, local)
+        if rank == 0:
+            print(json.dumps(res), flush=True)
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+        return 0
     return run_ours(args)
 
 

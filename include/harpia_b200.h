@@ -203,6 +203,30 @@ int32_t hb_apply_device(const hb_volume* in, hb_volume* out,
                         int64_t z_begin, void* stream, int32_t synchronize,
                         hb_report* rep);
 
+/* Multi-device streaming executor (SURVEY.md §8(b) "ndev, devices[]"): the
+ * plan's chunks are split into ndev contiguous z-slab groups (balanced by
+ * interior slices) and each group is streamed by hb_run's loop on its own
+ * device from its own host thread — one PCIe link per device, no device-to-
+ * device exchange (halos at group faces are read from the host volume, plan
+ * invariance keeps the stitched result identical to hb_run's).  `ex` is used
+ * for every group (its `device` is ignored; `cancel` must be thread-safe);
+ * failed_chunk is the global chunk index; `per_device` (optional, ndev
+ * entries) receives each group's report.  Replaces the sequential chunk loop
+ * of execute_chunked (chunking.py:242-274) when several B200s share a host. */
+int32_t hb_run_multi(const hb_volume* in, hb_volume* out,
+                     const hb_stage* stages, int32_t nstages,
+                     const hb_chunk* chunks, int64_t nchunks,
+                     const hb_exec* ex, int32_t ndev, const int32_t* devices,
+                     hb_report* rep, hb_report* per_device);
+
+/* Library-pool device buffers (extension): stream-ordered allocation from the
+ * same private cudaMemPool the executor uses, so z-slab buffers of a sharded
+ * job (ghost slices + interior) are reported by hb_device_pool_bytes and
+ * released by hb_trim_device / hb_session_end — never PyTorch's caching
+ * allocator.  HB_EBUDGET_SMALL when the device is out of memory. */
+int32_t hb_device_alloc(int32_t dev, int64_t bytes, void* stream, void** ptr);
+int32_t hb_device_free(int32_t dev, void* ptr, void* stream);
+
 /* Output dtype of a chain for a given input dtype (hb_dtype), or -1. */
 int32_t hb_chain_out_dtype(const hb_stage* stages, int32_t nstages, int32_t in_dtype);
 

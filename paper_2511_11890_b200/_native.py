@@ -157,6 +157,15 @@ def load() -> ctypes.CDLL:
                                       ctypes.POINTER(HbStage), i32, i64, vp, i32,
                                       ctypes.POINTER(HbReport)]
         L.hb_apply_device.restype = i32
+        L.hb_run_multi.argtypes = [ctypes.POINTER(HbVolume), ctypes.POINTER(HbVolume),
+                                   ctypes.POINTER(HbStage), i32, ctypes.POINTER(HbChunk), i64,
+                                   ctypes.POINTER(HbExec), i32, ctypes.POINTER(i32),
+                                   ctypes.POINTER(HbReport), ctypes.POINTER(HbReport)]
+        L.hb_run_multi.restype = i32
+        L.hb_device_alloc.argtypes = [i32, i64, vp, ctypes.POINTER(vp)]
+        L.hb_device_alloc.restype = i32
+        L.hb_device_free.argtypes = [i32, vp, vp]
+        L.hb_device_free.restype = i32
         L.hb_trim_device.argtypes = [i32]
         L.hb_trim_device.restype = i32
         L.hb_device_pool_bytes.argtypes = [i32]
@@ -324,8 +333,10 @@ def run_host(data: np.ndarray, out: np.ndarray, program: DeviceProgram,
              chunks: Sequence[tuple[int, int, int, int]], *, device: Optional[int] = None,
              cancel: Optional[Callable[[], bool]] = None, device_budget: int = 0,
              pipeline_depth: int = 0, fault_chunk: int = -1,
-             host_threads: int = 0) -> NativeReport:
-    """hb_run: stream host volume ``data`` through ``program`` chunk by chunk."""
+             host_threads: int = 0, devices: Optional[Sequence[int]] = None) -> NativeReport:
+    """hb_run: stream host volume ``data`` through ``program`` chunk by chunk.
+    ``devices`` (several ordinals): hb_run_multi, one z-slab group of chunks
+    per device, streamed concurrently."""
     L = load()
     if data.dtype not in DTYPE_CODE or out.dtype not in DTYPE_CODE:
         raise UnsupportedFormatError(f"unsupported dtype {data.dtype} -> {out.dtype}")
@@ -355,8 +366,13 @@ def run_host(data: np.ndarray, out: np.ndarray, program: DeviceProgram,
         ex.cancel = cb
     vin, vout = _host_volume(data), _host_volume(out)
     rep = HbReport()
-    rc = L.hb_run(ctypes.byref(vin), ctypes.byref(vout), m.arr, m.n, carr, nch,
-                  ctypes.byref(ex), ctypes.byref(rep))
+    if devices is not None and len(devices) > 1:
+        devs = (ctypes.c_int32 * len(devices))(*[int(d) for d in devices])
+        rc = L.hb_run_multi(ctypes.byref(vin), ctypes.byref(vout), m.arr, m.n, carr, nch,
+                            ctypes.byref(ex), len(devices), devs, ctypes.byref(rep), None)
+    else:
+        rc = L.hb_run(ctypes.byref(vin), ctypes.byref(vout), m.arr, m.n, carr, nch,
+                      ctypes.byref(ex), ctypes.byref(rep))
     if rc != HB_OK:
         raise_for_status(rc, rep.message.decode(errors="replace"),
                          failed_chunk=rep.failed_chunk, minimum_bytes=rep.minimum_bytes)
@@ -403,6 +419,74 @@ def apply_device(inp, out, program: DeviceProgram, z_begin: int = 0, stream=None
         raise_for_status(rc, rep.message.decode(errors="replace"),
                          failed_chunk=rep.failed_chunk, minimum_bytes=rep.minimum_bytes)
     return int(rep.kernel_launches)
+
+
+class DeviceBuffer:
+    """A device buffer from the library's private pool (hb_device_alloc),
+    exposed to torch through ``__cuda_array_interface__`` so tensors view it
+    without PyTorch's caching allocator.  Freed (stream-ordered on ``stream``)
+    by :meth:`free` or when garbage-collected."""
+
+    _TYPESTR = {"float32": "<f4", "uint16": "<u2", "uint8": "|u1", "uint32": "<u4",
+                "float64": "<f8", "int32": "<i4", "int64": "<i8"}
+
+    def __init__(self, shape, dtype, device: int, stream=None):
+        L = load()
+        self.shape = tuple(int(v) for v in shape)
+        self.dtype = np.dtype(dtype)
+        self.device = int(device)
+        self.stream = stream
+        nbytes = int(np.prod(self.shape, dtype=np.int64)) * self.dtype.itemsize
+        ptr = ctypes.c_void_p(0)
+        rc = L.hb_device_alloc(self.device, nbytes, ctypes.c_void_p(_stream_handle(stream)),
+                               ctypes.byref(ptr))
+        if rc != HB_OK:
+            raise_for_status(rc, last_error(), minimum_bytes=nbytes)
+        self.ptr = int(ptr.value or 0)
+        self.nbytes = nbytes
+
+    @property
+    def __cuda_array_interface__(self):
+        return {"shape": self.shape, "typestr": self._TYPESTR[self.dtype.name],
+                "data": (self.ptr, False), "version": 3, "strides": None,
+                "stream": None}
+
+    def tensor(self):
+        """A torch tensor viewing this buffer (keeps the buffer alive)."""
+        import torch
+
+        t = torch.as_tensor(self, device=f"cuda:{self.device}")
+        t._hb_owner = self  # lifetime: the buffer lives as long as the view
+        return t
+
+    def free(self, stream=None):
+        if self.ptr:
+            load().hb_device_free(self.device, ctypes.c_void_p(self.ptr),
+                                  ctypes.c_void_p(_stream_handle(stream if stream is not None
+                                                                 else self.stream)))
+            self.ptr = 0
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def _stream_handle(stream) -> int:
+    if stream is None:
+        try:
+            import torch
+
+            return int(torch.cuda.current_stream().cuda_stream)
+        except Exception:
+            return 0
+    return int(stream.cuda_stream if hasattr(stream, "cuda_stream") else stream)
+
+
+def device_empty(shape, dtype, device: int, stream=None):
+    """torch tensor on a library-pool buffer (see :class:`DeviceBuffer`)."""
+    return DeviceBuffer(shape, dtype, device, stream).tensor()
 
 
 def trim_device(dev: Optional[int] = None) -> None:

@@ -1498,13 +1498,11 @@ int32_t hb_apply_device(const hb_volume* in, hb_volume* out, const hb_stage* sta
   return HB_OK;
 }
 
-int32_t hb_run(const hb_volume* in, hb_volume* out, const hb_stage* stages, int32_t nstages,
-               const hb_chunk* chunks, int64_t nchunks, const hb_exec* ex, hb_report* rep) {
-  hb_report dummy;
-  if (!rep) rep = &dummy;
-  std::memset(rep, 0, sizeof(*rep));
-  rep->failed_chunk = -1;
-  const double t_start = now_ms();
+// Argument / plan validation shared by hb_run and hb_run_multi: the chunk
+// interiors must partition [0, Z) with halos inside the volume.
+static int32_t check_run(const hb_volume* in, hb_volume* out, const hb_stage* stages,
+                         int32_t nstages, const hb_chunk* chunks, int64_t nchunks,
+                         const hb_exec* ex, hb_report* rep, std::vector<StageDesc>& st) {
   if (!in || !out || !in->data || !out->data || !ex || !chunks) {
     set_err(rep, "null argument");
     return HB_EPARAM;
@@ -1518,7 +1516,6 @@ int32_t hb_run(const hb_volume* in, hb_volume* out, const hb_stage* stages, int3
     set_err(rep, "input/output shapes differ");
     return HB_EPARAM;
   }
-  std::vector<StageDesc> st;
   std::string msg;
   hb_status rc = normalise(stages, nstages, in->dtype, st, msg);
   if (rc != HB_OK) {
@@ -1546,6 +1543,18 @@ int32_t hb_run(const hb_volume* in, hb_volume* out, const hb_stage* stages, int3
     set_err(rep, "chunk interiors do not cover the volume");
     return HB_EPARAM;
   }
+  (void)max_int;
+  return HB_OK;
+}
+
+// The streaming loop over a run of plan chunks on ONE device (ex->device).
+static int32_t run_host_range(const hb_volume* in, hb_volume* out,
+                              const std::vector<StageDesc>& st, const hb_chunk* chunks,
+                              int64_t nchunks, const hb_exec* ex, hb_report* rep,
+                              double t_start) {
+  int64_t max_int = 0;
+  for (int64_t k = 0; k < nchunks; k++)
+    max_int = std::max(max_int, chunks[k].z_stop - chunks[k].z_start);
   const int dev = ex->device;
   if (dev < 0 || dev >= hb_device_count()) {
     set_err(rep, "no CUDA device " + std::to_string(dev));
@@ -1817,6 +1826,132 @@ int32_t hb_run(const hb_volume* in, hb_volume* out, const hb_stage* stages, int3
                  t_loop - t_setup, now_ms() - t_loop, t_free - t_loop, t_trim - t_free,
                  now_ms() - t_trim);
   return status;
+}
+
+
+int32_t hb_run(const hb_volume* in, hb_volume* out, const hb_stage* stages, int32_t nstages,
+               const hb_chunk* chunks, int64_t nchunks, const hb_exec* ex, hb_report* rep) {
+  hb_report dummy;
+  if (!rep) rep = &dummy;
+  std::memset(rep, 0, sizeof(*rep));
+  rep->failed_chunk = -1;
+  const double t_start = now_ms();
+  std::vector<StageDesc> st;
+  int32_t rc = check_run(in, out, stages, nstages, chunks, nchunks, ex, rep, st);
+  if (rc != HB_OK) return rc;
+  return run_host_range(in, out, st, chunks, nchunks, ex, rep, t_start);
+}
+
+int32_t hb_run_multi(const hb_volume* in, hb_volume* out, const hb_stage* stages,
+                     int32_t nstages, const hb_chunk* chunks, int64_t nchunks,
+                     const hb_exec* ex, int32_t ndev, const int32_t* devices, hb_report* rep,
+                     hb_report* per_device) {
+  hb_report dummy;
+  if (!rep) rep = &dummy;
+  std::memset(rep, 0, sizeof(*rep));
+  rep->failed_chunk = -1;
+  const double t_start = now_ms();
+  if (ndev < 1 || !devices) {
+    set_err(rep, "hb_run_multi: ndev >= 1 devices required");
+    return HB_EPARAM;
+  }
+  std::vector<StageDesc> st;
+  int32_t rc = check_run(in, out, stages, nstages, chunks, nchunks, ex, rep, st);
+  if (rc != HB_OK) return rc;
+  for (int i = 0; i < ndev; i++)
+    if (devices[i] < 0 || devices[i] >= hb_device_count()) {
+      set_err(rep, "no CUDA device " + std::to_string(devices[i]));
+      return HB_EBUDGET_UNAVAILABLE;
+    }
+  // contiguous chunk groups with balanced interior slices: device i owns the
+  // chunks whose interior starts in [i*Z/ndev, (i+1)*Z/ndev) — a z-slab per
+  // device, each streamed through its own PCIe link; halos at group faces are
+  // read from host memory (the out-of-core rule)
+  std::vector<int64_t> first(ndev + 1, nchunks);
+  {
+    int g = 0;
+    first[0] = 0;
+    for (int64_t k = 0; k < nchunks; k++) {
+      while (g + 1 < ndev && chunks[k].z_start >= (in->nz * (g + 1)) / ndev) first[++g] = k;
+    }
+    for (int i = g + 1; i <= ndev; i++) first[i] = nchunks;
+  }
+  std::vector<hb_report> reps(ndev);
+  std::vector<hb_exec> exs(ndev);
+  std::vector<int32_t> codes(ndev, HB_OK);
+  std::vector<std::thread> th;
+  for (int i = 0; i < ndev; i++) {
+    const int64_t k0 = first[i], n = first[i + 1] - first[i];
+    std::memset(&reps[i], 0, sizeof(hb_report));
+    reps[i].failed_chunk = -1;
+    if (n <= 0) continue;
+    exs[i] = *ex;
+    exs[i].device = devices[i];
+    exs[i].chunk_seconds = ex->chunk_seconds ? ex->chunk_seconds + k0 : nullptr;
+    exs[i].fault_chunk = ex->fault_chunk >= k0 && ex->fault_chunk < k0 + n ? (int32_t)(ex->fault_chunk - k0) : -1;
+    th.emplace_back([&, i, k0, n] {
+      codes[i] = run_host_range(in, out, st, chunks + k0, n, &exs[i], &reps[i], now_ms());
+      if (codes[i] != HB_OK && reps[i].failed_chunk >= 0) reps[i].failed_chunk += k0;
+    });
+  }
+  for (auto& t : th) t.join();
+  int32_t status = HB_OK;
+  for (int i = 0; i < ndev; i++) {
+    const hb_report& r = reps[i];
+    rep->chunk_count += r.chunk_count;
+    rep->device_peak_bytes = std::max(rep->device_peak_bytes, r.device_peak_bytes);
+    rep->device_residual_bytes += r.device_residual_bytes;
+    rep->h2d_bytes += r.h2d_bytes;
+    rep->d2h_bytes += r.d2h_bytes;
+    rep->kernel_ms = std::max(rep->kernel_ms, r.kernel_ms);
+    rep->kernel_launches += r.kernel_launches;
+    if (codes[i] != HB_OK && status == HB_OK) {  // the lowest failing group reports
+      status = codes[i];
+      rep->failed_chunk = r.failed_chunk;
+      rep->minimum_bytes = r.minimum_bytes;
+      std::memcpy(rep->message, r.message, sizeof(rep->message));
+    }
+    if (per_device) per_device[i] = r;
+  }
+  rep->wall_ms = now_ms() - t_start;
+  if (status != HB_OK) set_err(nullptr, rep->message);
+  return status;
+}
+
+int32_t hb_device_alloc(int32_t dev, int64_t bytes, void* stream, void** ptr) {
+  if (!ptr || bytes < 0 || dev < 0 || dev >= hb_device_count()) {
+    set_err(nullptr, "hb_device_alloc: bad arguments");
+    return HB_EPARAM;
+  }
+  *ptr = nullptr;
+  cudaSetDevice(dev);
+  {
+    std::lock_guard<std::mutex> lk(g_dev[dev].mu);
+    cudaError_t e = ensure_pool(dev);
+    if (e == cudaSuccess)
+      e = cudaMallocFromPoolAsync(ptr, (size_t)std::max<int64_t>(bytes, 256), g_dev[dev].pool,
+                                  (cudaStream_t)stream);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      *ptr = nullptr;
+      set_err(nullptr, std::string("hb_device_alloc: ") + cudaGetErrorString(e));
+      return e == cudaErrorMemoryAllocation ? HB_EBUDGET_SMALL : HB_ECUDA;
+    }
+  }
+  return HB_OK;
+}
+
+int32_t hb_device_free(int32_t dev, void* ptr, void* stream) {
+  if (!ptr) return HB_OK;
+  if (dev < 0 || dev >= hb_device_count()) return HB_EPARAM;
+  cudaSetDevice(dev);
+  cudaError_t e = cudaFreeAsync(ptr, (cudaStream_t)stream);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    set_err(nullptr, std::string("hb_device_free: ") + cudaGetErrorString(e));
+    return HB_ECUDA;
+  }
+  return HB_OK;
 }
 
 }  // extern "C"

@@ -17,15 +17,22 @@ Two ways to obtain the ghost slices:
   (NVLink/NVSwitch), i.e. halo slices of stage ``s`` output feed stage ``s+1``.
 
 One process per GPU; ``torch.distributed`` provides the plumbing (``nccl`` on
-B200, ``gloo`` in the CPU tests).  The per-block compute is injected
-(``apply_block``) so the exchange/stitching logic is testable without a GPU;
-the default is the device path (``_native.apply_device``).
+B200, ``gloo`` in the CPU tests).  Per stage the exchange is posted first and
+the slices that need no ghost data are computed while it is in flight; the
+boundary slices follow once the ghosts land.  Slabs live in padded buffers
+[ghost_lo | interior | ghost_hi] from the library's device pool, so ghosts
+are received in place and each stage writes the next stage's interior.  The
+per-block compute is injected (``apply_block``) so the exchange/stitching
+logic is testable without a GPU; the default is the device path
+(``_native.apply_device``).  ``run_sharded_local`` runs the same schedule for
+several slabs held by one process (virtual ranks; tested on one B200).
 """
 
 from __future__ import annotations
 
 from dataclasses import dataclass
-from typing import Callable, Optional
+import time
+from typing import Callable, Optional, Sequence
 
 import numpy as np
 
@@ -62,67 +69,233 @@ def _dist():
     return dist
 
 
-def exchange_halos(local, halo: int, rank: int, world: int, group=None):
-    """Return (padded, lo, hi): ``local`` (Zr, Y, X) extended with up to
-    ``halo`` slices received from each neighbour.  ``lo``/``hi`` are the ghost
-    slices actually present (0 at the global faces, where the operator clamps
-    exactly as the reference does at volume faces).
-    """
+# ---------------------------------------------------------------------------
+# Padded slab buffers: [ghost_lo | interior | ghost_hi] in ONE contiguous
+# (lo + n + hi, Y, X) buffer, so received halo slices land in place (no
+# torch.cat) and a stage's output is written straight into the interior of
+# the next stage's buffer.  On the device the buffer comes from the library's
+# private pool (hb_device_alloc), never from PyTorch's caching allocator.
+# ---------------------------------------------------------------------------
+def _empty(shape, dtype, like):
     import torch
 
-    if halo == 0 or world == 1:
-        return local, 0, 0
-    if local.shape[0] < halo:
-        raise ValueError(f"slab of {local.shape[0]} slices is thinner than the halo {halo}")
-    dist = _dist()
-    ops = []
-    lo_buf = hi_buf = None
-    if rank > 0:
-        lo_buf = torch.empty((halo,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
-        ops.append(dist.P2POp(dist.irecv, lo_buf, rank - 1, group))
-        ops.append(dist.P2POp(dist.isend, local[:halo].contiguous(), rank - 1, group))
-    if rank < world - 1:
-        hi_buf = torch.empty((halo,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
-        ops.append(dist.P2POp(dist.isend, local[-halo:].contiguous(), rank + 1, group))
-        ops.append(dist.P2POp(dist.irecv, hi_buf, rank + 1, group))
-    for req in dist.batch_isend_irecv(ops):
-        req.wait()
-    parts = [p for p in (lo_buf, local, hi_buf) if p is not None]
-    padded = torch.cat(parts, dim=0) if len(parts) > 1 else local
-    return padded, (halo if lo_buf is not None else 0), (halo if hi_buf is not None else 0)
+    if like.device.type == "cuda":
+        from . import _native
+
+        np_dt = np.dtype(str(dtype).replace("torch.", ""))
+        return _native.device_empty(shape, np_dt, like.device.index or 0)
+    return torch.empty(shape, dtype=dtype, device=like.device)
 
 
-def _device_apply(block, program, z_begin: int, nz_out: int):
-    import torch
+@dataclass
+class PaddedSlab:
+    buf: object   # (lo + n + hi, Y, X) tensor
+    lo: int       # ghost slices below (received from rank - 1)
+    hi: int       # ghost slices above (received from rank + 1)
 
+    @property
+    def n(self) -> int:
+        return self.buf.shape[0] - self.lo - self.hi
+
+    @property
+    def interior(self):
+        return self.buf[self.lo:self.lo + self.n]
+
+
+def alloc_padded(n: int, plane: tuple, dtype, like, lo: int, hi: int) -> PaddedSlab:
+    return PaddedSlab(_empty((lo + n + hi,) + tuple(plane), dtype, like), lo, hi)
+
+
+class DistTransport:
+    """Neighbour halo exchange over torch.distributed P2P (NCCL over
+    NVLink/NVSwitch on the B200 box — one ncclSend/ncclRecv pair per face,
+    batched; gloo in the CPU tests).  ``start`` posts the sends of this
+    rank's first/last ``h`` interior slices and the receives into its ghost
+    slices and returns at once; ``finish`` makes the compute stream (NCCL) or
+    the host (gloo) wait for them."""
+
+    def __init__(self, rank: int, world: int, group=None):
+        self.rank, self.world, self.group = rank, world, group
+
+    def start(self, slab: PaddedSlab, h: int):
+        dist = _dist()
+        ops, r, g = [], self.rank, self.group
+        if h == 0 or self.world == 1:
+            return []
+        inner = slab.interior
+        if r > 0:
+            ops.append(dist.P2POp(dist.irecv, slab.buf[slab.lo - h:slab.lo], r - 1, g))
+            ops.append(dist.P2POp(dist.isend, inner[:h], r - 1, g))
+        if r < self.world - 1:
+            ops.append(dist.P2POp(dist.isend, inner[inner.shape[0] - h:], r + 1, g))
+            ops.append(dist.P2POp(dist.irecv, slab.buf[slab.lo + slab.n:slab.lo + slab.n + h], r + 1, g))
+        return dist.batch_isend_irecv(ops)
+
+    def finish(self, pending) -> None:
+        for req in pending:
+            req.wait()
+
+    def min_slab(self, n: int, like) -> int:
+        """Smallest slab over all ranks (every rank must hold >= halo slices
+        for its neighbours' ghosts; checked collectively before any P2P op)."""
+        import torch
+
+        if self.world == 1:
+            return n
+        dist = _dist()
+        dev = _comm_device(self.group)
+        t = torch.tensor([n], dtype=torch.int64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN, group=self.group)
+        return int(t.item())
+
+
+def _device_apply(block, program, z_begin: int, out) -> None:
+    """Apply ``program`` to device ``block`` (clamp at its faces), writing
+    block slices [z_begin, z_begin + len(out)) into ``out``."""
     from . import _native
 
-    out_dt = program.out_dtype(np.dtype(str(block.dtype).replace("torch.", "")))
-    out = torch.empty((nz_out,) + tuple(block.shape[1:]), dtype=getattr(torch, out_dt.name),
-                      device=block.device)
     _native.apply_device(block, out, program, z_begin)
-    return out
 
 
-def run_sharded(local, program, rank: int, world: int, group=None,
-                apply_block: Optional[Callable] = None, per_stage: bool = True):
+def _pieces(a: int, b: int, step: int):
+    z = a
+    while z < b:
+        yield z, min(b, z + step)
+        z += step
+
+
+def _apply_range(src: PaddedSlab, a: int, b: int, h: int, program, dst, apply_block,
+                 piece: int) -> None:
+    """Outputs for interior slices [a, b) of ``src`` into dst[a:b], in z-pieces
+    of <= ``piece`` slices (bounded device scratch).  Each piece's block is the
+    padded buffer's [a - h, b + h) clipped to what the buffer holds; faces of a
+    clipped block are real volume faces, where the operator clamps exactly as
+    the reference does."""
+    P = src.buf.shape[0]
+    for pa, pb in _pieces(a, b, piece):
+        b0 = max(0, src.lo + pa - h)
+        b1 = min(P, src.lo + pb + h)
+        apply_block(src.buf[b0:b1], program, src.lo + pa - b0, dst[pa:pb])
+
+
+def run_sharded(local, program, rank: int, world: int, group=None,  # local: tensor | PaddedSlab
+                apply_block: Optional[Callable] = None, per_stage: bool = True,
+                transport=None, piece_slices: Optional[int] = None, timings: Optional[dict] = None):
     """Apply ``program`` to a z-sharded volume; returns this rank's interior output.
 
     per_stage=True: one halo exchange per chained stage (stage s+1's ghosts are
     stage s outputs), so no slice is computed twice.  per_stage=False: one
     exchange of the chain's total halo, then the whole chain on the padded slab.
+
+    Per stage: post the exchange, compute the slices that need no ghost data
+    (the interior [h, n - h), or up to the volume face on the first / last
+    rank) while it is in flight, then the boundary slices once it lands
+    (SURVEY.md §8(e) interior-first overlap).  Outputs are written into the
+    next stage's padded buffer in place.
     """
     from . import _native
 
     apply_block = apply_block or _device_apply
-    stages = program.stages if per_stage else [None]
-    cur = local
-    for st in stages:
-        prog = _native.DeviceProgram([st]) if st is not None else program
-        h = prog.halo()
-        padded, lo, hi = exchange_halos(cur, h, rank, world, group)
-        cur = apply_block(padded, prog, lo, padded.shape[0] - lo - hi)
-    return cur
+    transport = transport or DistTransport(rank, world, group)
+    stages = [_native.DeviceProgram([st]) for st in program.stages] if per_stage else [program]
+    halos = [p.halo() for p in stages]
+    given = local if isinstance(local, PaddedSlab) else None
+    if given is not None:
+        local = given.interior
+    n = int(local.shape[0])
+    plane = tuple(local.shape[1:])
+    # every rank checks together: a neighbour thinner than the halo would leave
+    # ghosts incomplete (and a one-sided error would hang the P2P exchange)
+    need = max(halos) if world > 1 else 0
+    if need and transport.min_slab(n, local) < need:
+        raise ValueError(f"a z-slab is thinner than the halo {need}: use fewer ranks")
+    if piece_slices is None:
+        itemsize = max(local.element_size(), 4)
+        piece_slices = max(1, int((2 << 30) // max(1, itemsize * plane[0] * plane[1])))
+    lo = [h if rank > 0 else 0 for h in halos]
+    hi = [h if rank < world - 1 else 0 for h in halos]
+    in_dt = np.dtype(str(local.dtype).replace("torch.", ""))
+    if given is not None and given.lo == lo[0] and given.hi == hi[0]:
+        cur = given  # caller built the slab in a padded buffer: no copy
+    else:
+        cur = alloc_padded(n, plane, local.dtype, local, lo[0], hi[0])
+        cur.interior.copy_(local)
+    xchg_s = 0.0
+    for k, (prog, h) in enumerate(zip(stages, halos)):
+        out_np = prog.out_dtype(in_dt)
+        import torch
+
+        out_dt = getattr(torch, out_np.name)
+        last = k + 1 == len(stages)
+        nxt = (alloc_padded(n, plane, out_dt, local, 0, 0) if last
+               else alloc_padded(n, plane, out_dt, local, lo[k + 1], hi[k + 1]))
+        dst = nxt.interior
+        t0 = time.perf_counter()
+        pending = transport.start(cur, h) if (world > 1 and h > 0) else []
+        a, b = lo[k], n - hi[k]  # needs no ghost data
+        if a < b:
+            _apply_range(cur, a, b, h, prog, dst, apply_block, piece_slices)
+        transport.finish(pending)
+        xchg_s += time.perf_counter() - t0
+        if a >= b:
+            _apply_range(cur, 0, n, h, prog, dst, apply_block, piece_slices)
+        else:
+            if a > 0:
+                _apply_range(cur, 0, a, h, prog, dst, apply_block, piece_slices)
+            if b < n:
+                _apply_range(cur, b, n, h, prog, dst, apply_block, piece_slices)
+        cur = nxt
+        in_dt = out_np
+    if timings is not None:
+        timings["exchange_host_s"] = xchg_s
+    return cur.interior
+
+
+def run_sharded_local(slabs: Sequence, program, per_stage: bool = True,
+                      apply_block: Optional[Callable] = None, piece_slices: Optional[int] = None):
+    """Several z-slabs of one volume held by ONE process (e.g. virtual ranks on
+    one GPU, or a C-style multi-device caller): the same per-stage schedule as
+    :func:`run_sharded` with ghost slices copied device-to-device.  Returns the
+    per-slab outputs; their concatenation equals the single-volume result."""
+    from . import _native
+    import torch
+
+    apply_block = apply_block or _device_apply
+    world = len(slabs)
+    stages = [_native.DeviceProgram([st]) for st in program.stages] if per_stage else [program]
+    halos = [p.halo() for p in stages]
+    if world > 1 and min(int(s.shape[0]) for s in slabs) < max(halos):
+        raise ValueError(f"a z-slab is thinner than the halo {max(halos)}")
+    ns = [int(s.shape[0]) for s in slabs]
+    plane = tuple(slabs[0].shape[1:])
+    in_dt = np.dtype(str(slabs[0].dtype).replace("torch.", ""))
+    if piece_slices is None:
+        piece_slices = max(1, int((2 << 30) // max(1, 4 * plane[0] * plane[1])))
+    curs = []
+    for r, s in enumerate(slabs):
+        h0 = halos[0]
+        c = alloc_padded(ns[r], plane, s.dtype, s, h0 if r > 0 else 0, h0 if r < world - 1 else 0)
+        c.interior.copy_(s)
+        curs.append(c)
+    for k, (prog, h) in enumerate(zip(stages, halos)):
+        out_np = prog.out_dtype(in_dt)
+        out_dt = getattr(torch, out_np.name)
+        last = k + 1 == len(stages)
+        nh = 0 if last else halos[k + 1]
+        nxts = [alloc_padded(ns[r], plane, out_dt, slabs[r], 0 if (last or r == 0) else nh,
+                             0 if (last or r == world - 1) else nh) for r in range(world)]
+        # ghosts: rank r's lower ghosts = rank r-1's last h interior slices, etc.
+        for r in range(world):
+            c = curs[r]
+            if r > 0 and h:
+                c.buf[c.lo - h:c.lo].copy_(curs[r - 1].interior[ns[r - 1] - h:])
+            if r < world - 1 and h:
+                c.buf[c.lo + c.n:c.lo + c.n + h].copy_(curs[r + 1].interior[:h])
+        for r in range(world):
+            _apply_range(curs[r], 0, ns[r], h, prog, nxts[r].interior, apply_block, piece_slices)
+        curs = nxts
+        in_dt = out_np
+    return [c.interior for c in curs]
 
 
 # ---------------------------------------------------------------------------

@@ -25,9 +25,14 @@ def _free_port():
     return p
 
 
-def _oracle_apply(block, prog, z_begin, nz_out):
+def _oracle_apply(block, prog, z_begin, out):
     """apply_block for the CPU test: the oracle evaluates every stage on the
-    padded block (clamp at its faces) and the interior is returned."""
+    padded block (clamp at its faces) and writes block slices
+    [z_begin, z_begin + len(out)) into ``out``."""
+    out.copy_(_oracle_eval(block, prog, z_begin, out.shape[0]))
+
+
+def _oracle_eval(block, prog, z_begin, nz_out):
     sys.path.insert(0, ROOT)
     from oracle import oracle as O
     from paper_2511_11890_b200 import _native
@@ -75,7 +80,7 @@ def _program(name):
     raise KeyError(name)
 
 
-def _worker(rank, world, port, name, per_stage, outdir):
+def _worker(rank, world, port, name, per_stage, outdir, piece=None):
     sys.path.insert(0, ROOT)
     from paper_2511_11890_b200 import sharding
 
@@ -88,7 +93,7 @@ def _worker(rank, world, port, name, per_stage, outdir):
         me = slabs[rank]
         local = torch.from_numpy(np.ascontiguousarray(vol[me.z0:me.z1]))
         out = sharding.run_sharded(local, prog, rank, world, apply_block=_oracle_apply,
-                                   per_stage=per_stage)
+                                   per_stage=per_stage, piece_slices=piece)
         np.save(os.path.join(outdir, f"r{rank}.npy"), out.numpy())
     finally:
         dist.destroy_process_group()
@@ -106,9 +111,51 @@ def test_sharded_equals_whole(name, per_stage, world, oracle):
     with tempfile.TemporaryDirectory() as d:
         mp.spawn(_worker, args=(world, _free_port(), name, per_stage, d), nprocs=world, join=True)
         got = np.concatenate([np.load(os.path.join(d, f"r{r}.npy")) for r in range(world)])
-    whole = _oracle_apply(torch.from_numpy(vol), prog, 0, vol.shape[0]).numpy()
+    whole = _oracle_eval(torch.from_numpy(vol), prog, 0, vol.shape[0]).numpy()
     assert got.dtype == whole.dtype
     assert np.array_equal(got, whole)
+
+
+def test_sharded_small_pieces_equal_whole(oracle):
+    """interior-first schedule with 2-slice compute pieces (many clipped blocks)."""
+    prog, kind = _program("unsharp_log")
+    vol = _volume(kind)
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_worker, args=(2, _free_port(), "unsharp_log", True, d, 2), nprocs=2, join=True)
+        got = np.concatenate([np.load(os.path.join(d, f"r{r}.npy")) for r in range(2)])
+    whole = _oracle_eval(torch.from_numpy(vol), prog, 0, vol.shape[0]).numpy()
+    assert np.array_equal(got, whole)
+
+
+def _thin_worker(rank, world, port, outdir):
+    sys.path.insert(0, ROOT)
+    from paper_2511_11890_b200 import filters, sharding
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    try:
+        vol = np.zeros((10, 4, 4), np.float32)
+        me = sharding.partition(10, world)[rank]  # 3, 3, 2, 2 slices
+        local = torch.from_numpy(np.ascontiguousarray(vol[me.z0:me.z1]))
+        try:
+            sharding.run_sharded(local, filters.median_program(3), rank, world,
+                                 apply_block=_oracle_apply)
+            msg = "no error"
+        except ValueError as exc:
+            msg = str(exc)
+        with open(os.path.join(outdir, f"e{rank}.txt"), "w") as f:
+            f.write(msg)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_thin_slab_fails_on_every_rank():
+    """A slab thinner than the halo raises on ALL ranks before any P2P op
+    (no rank is left waiting in the exchange)."""
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_thin_worker, args=(4, _free_port(), d), nprocs=4, join=True)
+        msgs = [open(os.path.join(d, f"e{r}.txt")).read() for r in range(4)]
+    assert all("thinner than the halo" in m for m in msgs), msgs
 
 
 def test_partition():
