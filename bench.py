@@ -102,10 +102,13 @@ class Clocks:
             # CUDA ordinal -> NVML handle via PCI bus id
             import torch
 
-            bus = torch.cuda.get_device_properties(self.index).pci_bus_id \
-                if hasattr(torch.cuda.get_device_properties(self.index), "pci_bus_id") else None
-            self.h = (nv.nvmlDeviceGetHandleByPciBusId(bus) if bus
-                      else nv.nvmlDeviceGetHandleByIndex(self.index))
+            pr = torch.cuda.get_device_properties(self.index)
+            dom, bus, dev = (getattr(pr, k, None) for k in ("pci_domain_id", "pci_bus_id",
+                                                           "pci_device_id"))
+            if all(isinstance(v, int) for v in (dom, bus, dev)):
+                self.h = nv.nvmlDeviceGetHandleByPciBusId(f"{dom:08x}:{bus:02x}:{dev:02x}.0")
+            else:
+                self.h = nv.nvmlDeviceGetHandleByIndex(self.index)
             self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
             self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
@@ -289,7 +292,7 @@ def run_reference(args):
 # --------------------------------------------------------------------------
 # GPU arm
 # --------------------------------------------------------------------------
-KERNEL_NAMES = {"gaussian": "k_gauss_p2<8,float>", "median": "k_median3_plane<float>"}
+KERNEL_NAMES = {"gaussian": "k_gauss_ws<8,float,64>", "median": "k_median3_plane<float>"}
 
 
 def run_ours(args):

@@ -841,6 +841,12 @@ cudaError_t gaussian_fused(const DevIn& in, int64_t zo, int64_t nzo, float* out,
   if (!envelope_ok(in, nzo) || taps.R > 8) return cudaErrorNotSupported;
   cudaError_t e = cudaErrorNotSupported;
   if (epi.kind == EPI_UNSHARP && (epi.orig != in.p || epi.orig_dt != in.dt)) return cudaErrorNotSupported;
+  // warp-specialised kernel first (HB_GAUSS_P2=1: the single-role packed one)
+  if (taps.R >= 2 && !std::getenv("HB_GAUSS_SCALAR")) {
+    e = gaussian_ws(in, zo, nzo, out, taps, epi, s, launches);
+    if (e != cudaErrorNotSupported) return e;
+    cudaGetLastError();
+  }
   // packed-FP32 kernel for R >= 2 (HB_GAUSS_SCALAR=1 selects the scalar one)
   if (taps.R >= 2 && !std::getenv("HB_GAUSS_SCALAR")) {
     e = epi.kind == EPI_UNSHARP ? dispatch_p2_dt<true>(taps.R, in, zo, nzo, out, taps, epi, s)
