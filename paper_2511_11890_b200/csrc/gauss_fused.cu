@@ -843,6 +843,9 @@ cudaError_t gaussian_fused(const DevIn& in, int64_t zo, int64_t nzo, float* out,
   if (epi.kind == EPI_UNSHARP && (epi.orig != in.p || epi.orig_dt != in.dt)) return cudaErrorNotSupported;
   // warp-specialised kernel first (HB_GAUSS_P2=1: the single-role packed one)
   if (taps.R >= 2 && !std::getenv("HB_GAUSS_SCALAR")) {
+    e = gaussian_tri(in, zo, nzo, out, taps, epi, s, launches);
+    if (e != cudaErrorNotSupported) return e;
+    cudaGetLastError();
     e = gaussian_ws(in, zo, nzo, out, taps, epi, s, launches);
     if (e != cudaErrorNotSupported) return e;
     cudaGetLastError();

@@ -99,6 +99,24 @@ def test_gaussian_zsplit_vs_oracle(torch_dev, oracle, shape):
     assert float_close(u, refu) <= FLOAT_TOL
 
 
+def test_gaussian_tri_ragged_vs_oracle(torch_dev, oracle):
+    """k_gauss_tri (sigma = 2 on planes >= 384^2): ragged x / y tiles (406 =
+    8 x 48 + 22, 398 = 12 x 32 + 14), several capped z-chunks (nzo = 230 >
+    192) and the unsharp epilogue, against the oracle."""
+    from paper_2511_11890_b200 import filters
+
+    torch = torch_dev
+    rng = np.random.default_rng(406)
+    xh = rng.random((230 + 16, 398, 406), dtype=np.float32)
+    x = torch.from_numpy(xh).cuda()
+    ref = oracle.gaussian(xh, 2.0)[8:-8]
+    fast = _apply(torch, x, filters.gaussian_program(2.0, "fast"), 8).cpu().numpy()
+    assert float_close(fast, ref) <= FLOAT_TOL
+    refu = oracle.unsharp(xh, 2.0, 1.5)[8:-8]
+    u = _apply(torch, x, filters.unsharp_program(2.0, 1.5, "fast"), 8).cpu().numpy()
+    assert float_close(u, refu) <= FLOAT_TOL
+
+
 @pytest.mark.parametrize("sigma", [2.5, 3.3])
 def test_gaussian_large_sigma_vs_oracle(torch_dev, oracle, sigma):
     """R = ceil(4 sigma) > 8: the generic separable path, fast and exact."""
