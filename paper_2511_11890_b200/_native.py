@@ -117,6 +117,7 @@ EXPORTS = (
     "hb_device_pool_bytes", "hb_pin", "hb_unpin", "hb_last_error",
     "hb_session_begin", "hb_session_end", "hb_minmax", "hb_histogram",
     "hb_connected_components", "hb_label_filter", "hb_geodesic", "hb_edt", "hb_plan",
+    "hb_run_multi", "hb_device_alloc", "hb_device_free",
 )
 
 _lock = threading.Lock()
