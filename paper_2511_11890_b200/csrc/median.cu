@@ -7,6 +7,7 @@
 //           discards the min and max of the set and admits one new sample).
 // r >= 3:   per-voxel radix (bit-by-bit) selection over order-preserving keys.
 #include <algorithm>
+#include <type_traits>
 #include <cstdlib>
 
 #include "ops.cuh"
@@ -789,6 +790,11 @@ cudaError_t run_median(const DevIn& in, int64_t zo, int64_t nzo, void* out, int 
   const T* src = (const T*)in.p;
   T* dst = (T*)out;
   if (r == 1) {
+    if constexpr (std::is_same<T, float>::value) {
+      const cudaError_t e = median3_f32(in, zo, nzo, (float*)out, s, launches);
+      if (e != cudaErrorNotSupported) return e;
+      cudaGetLastError();
+    }
     dim3 grid((unsigned)((in.nx + M3_TX - 1) / M3_TX), (unsigned)((in.ny + M3_TY - 1) / M3_TY), 1);
     const int64_t tiles = (int64_t)grid.x * grid.y;
     // z-chunk: enough CTAs that the wave tail is small (3 CTAs/SM resident),

@@ -148,6 +148,10 @@ cudaError_t label_filter(const void* in, int dt, int64_t nz, int64_t ny, int64_t
                          cudaStream_t s);
 
 // --- median (median.cu) ----------------------------------------------------
+// r = 1 on float32 through the TMA-fed kernel (median3f.cu); NotSupported
+// outside its envelope
+cudaError_t median3_f32(const DevIn& in, int64_t zo, int64_t nzo, float* out, cudaStream_t s,
+                        int64_t* launches);
 cudaError_t median(const DevIn& in, int64_t zo, int64_t nzo, void* out, int r,
                    cudaStream_t s, int64_t* launches);
 
