@@ -12,7 +12,10 @@
 //     maximum of a compare-exchange is a + b - min on the raw bit patterns
 //     (IMAD, exact mod 2^32: min is one of the two inputs), which moves half
 //     of every compare-exchange to the FMA pipe;
-//   * 32-bit per-CTA bookkeeping, STG.64 stores.
+//   * 32-bit per-CTA bookkeeping, predicated STG.64 stores;
+//   * the 3x3 tableau's exchanges in min/max (ALU-only) form: the kernel is
+//     issue-bound with ALU-pipe headroom, and an ALU exchange is 2 issue
+//     slots against 3 (1024^3: 231 -> 244 Gvox/s).
 // The TMA box starts 16-B aligned at x0 - 4 (a misaligned start coordinate
 // faults), so a thread reads its x-1 .. x+2 columns as three LDS.64.
 #include <cuda.h>
@@ -28,6 +31,9 @@
 namespace hb {
 namespace {
 
+#ifndef HB_M3_ALU_EVERY
+#define HB_M3_ALU_EVERY 0  // merge exchanges in ALU form: 1, 2, 3 measured 226, 238, 240 vs 244 Gvox/s at 0
+#endif
 constexpr int TXO = 64, TYO = 8;       // outputs per CTA slice (32 x-pairs x 8 rows)
 constexpr int SW = 72, SH = TYO + 2;   // staged box: columns x0-4 .. x0+67, rows y0-1 .. y0+8
 constexpr int NST = 6;                 // TMA stages
@@ -65,6 +71,14 @@ struct NetF {
     b = imad(lo, mone, s);
     a = lo;
   }
+  // compare-exchange entirely on the ALU pipe (2 issue slots instead of 3):
+  // the kernel is issue-bound with ALU-pipe headroom (ncu: issue 84%, ALU
+  // 67%), so a share of the exchanges use this form
+  __device__ __forceinline__ void ce_alu(int& a, int& b) const {
+    const int lo = fmn(a, b);
+    b = fmx(a, b);
+    a = lo;
+  }
   __device__ __forceinline__ void sort3(int& a, int& b, int& c) const {
     const int lo = fmn3(a, b, c);
     const int hi = fmx3(a, b, c);
@@ -79,8 +93,8 @@ struct NetF {
   __device__ __forceinline__ void tableau(const int (&m)[3][3], int (&s)[9]) const {
     s[0] = m[0][0]; s[1] = m[0][1]; s[2] = m[1][0]; s[3] = m[0][2]; s[4] = m[1][1];
     s[5] = m[2][0]; s[6] = m[1][2]; s[7] = m[2][1]; s[8] = m[2][2];
-    ce(s[3], s[5]); ce(s[1], s[2]); ce(s[2], s[3]); ce(s[6], s[7]);
-    ce(s[5], s[6]); ce(s[3], s[4]); ce(s[4], s[5]);
+    ce_alu(s[3], s[5]); ce_alu(s[1], s[2]); ce_alu(s[2], s[3]); ce_alu(s[6], s[7]);
+    ce_alu(s[5], s[6]); ce_alu(s[3], s[4]); ce_alu(s[4], s[5]);
   }
   // sorted planes of the two x-adjacent outputs from r[row][x-1 .. x+2]
   __device__ __forceinline__ void planes2(int (&r)[3][4], int (&pa)[9], int (&pb)[9]) const {
@@ -105,7 +119,9 @@ struct NetF {
       w[i] = cur[i];
       w[9 + i] = nxt[i];
     }
-#define HB_CE(i, j) ce(w[i], w[j]);
+    int nce = 0;  // compile-time after unrolling: every HB_M3_ALU_EVERY-th exchange in ALU form
+#define HB_CE(i, j) \
+  if (HB_M3_ALU_EVERY > 0 && (nce++ % HB_M3_ALU_EVERY) == 0) ce_alu(w[i], w[j]); else ce(w[i], w[j]);
 #define HB_MN(i, j) w[i] = fmn(w[i], w[j]);
 #define HB_MX(i, j) w[j] = fmx(w[i], w[j]);
     HB_MERGE9_RANK4_13(HB_CE, HB_MN, HB_MX)
@@ -210,13 +226,17 @@ k_median3_f32(const __grid_constant__ CUtensorMap tin, float* __restrict__ out,
     ++k;
     net.planes2(r, pa, pb);
   };
+  // predicated stores (no divergent branch around them)
+  const bool single0 = !pair_store && st_y && st_x0, single1 = !pair_store && st_y && st_x1;
   auto emit = [&](int m0, int m1) {
-    if (pair_store) {
-      *reinterpret_cast<float2*>(optr) = make_float2(__int_as_float(m0), __int_as_float(m1));
-    } else if (st_y) {
-      if (st_x0) optr[0] = __int_as_float(m0);
-      if (st_x1) optr[1] = __int_as_float(m1);
-    }
+    asm volatile(
+        "{\n.reg .pred p, q, r;\n"
+        "setp.ne.b32 p, %3, 0;\n setp.ne.b32 q, %4, 0;\n setp.ne.b32 r, %5, 0;\n"
+        "@p st.global.v2.b32 [%0], {%1, %2};\n"
+        "@q st.global.b32 [%0], %1;\n"
+        "@r st.global.b32 [%0+4], %2;\n}\n" ::"l"(optr),
+        "r"(m0), "r"(m1), "r"((int)pair_store), "r"((int)single0), "r"((int)single1)
+        : "memory");
     optr += plane;
   };
   int X[2][9], Y[2][9], Z[2][9], W[2][9], M[2][10];
