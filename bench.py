@@ -292,7 +292,7 @@ def run_reference(args):
 # --------------------------------------------------------------------------
 # GPU arm
 # --------------------------------------------------------------------------
-KERNEL_NAMES = {"gaussian": "k_gauss_ws<8,float,64>", "median": "k_median3_plane<float>"}
+KERNEL_NAMES = {"gaussian": "k_gauss_tri<8,false>", "median": "k_median3_f32"}
 
 
 def run_ours(args):

@@ -1,4 +1,4 @@
-"""One launch each of the headline kernels (gaussian sigma=2 fast, median r=1)
+"""One launch each of the headline kernels (gaussian sigma=2 fast, median r=1, mean r=1)
 on the bench's 1024^3 padded block, for ncu."""
 import sys
 
@@ -16,5 +16,7 @@ if "g" in which:
     _native.apply_device(x, o, filters.gaussian_program(2.0), 8, s)
 if "m" in which:
     _native.apply_device(x, o, filters.median_program(1), 8, s)
+if "M" in which:  # mean r=1 (the streaming box kernel)
+    _native.apply_device(x, o, filters.mean_program(1), 8, s)
 torch.cuda.synchronize()
 print('done')

@@ -35,7 +35,7 @@ METRICS = [
     ("smsp__average_warps_issue_stalled_short_scoreboard_per_issue_active.ratio", "stall short_scoreboard"),
 ]
 
-KEYS = {"k_median3_plane": "median", "k_box_stream": "mean", "k_gauss_p2<8": "gaussian",
+KEYS = {"k_median3_f32": "median", "k_gauss_tri<8": "gaussian", "k_median3_plane": "median_plane", "k_box_stream": "mean", "k_gauss_p2<8": "gaussian_p2", "k_gauss_ws<8": "gaussian_ws",
         "k_morph3": "erode", "k_log_stream": "log_stage2", "k_exact_z2<8": "exact_z",
         "k_exact_yx<8": "exact_yx"}
 
