@@ -861,6 +861,163 @@ cudaError_t launch_morph3_v(const DevIn& in, int64_t zo, int64_t nzo, void* out,
   return cudaGetLastError();
 }
 
+#ifndef HB_MB_TY
+#define HB_MB_TY 8  // output rows per thread
+#endif
+// ---------------------------------------------------------------------------
+// Binary {0,1} uint8 volumes (configs[2]'s binary case), ONE BIT per voxel in
+// registers: erosion is AND and dilation OR over the SE, so 32 voxels go
+// through every logic op.  A thread owns one 32-voxel word column x MB_TY
+// output rows and marches z:
+//   * each staged row is loaded as 32 bytes (2 x LDG.128, a warp reads 1 KB
+//     contiguous) and packed to a word with (v * 0x204081) >> 21 (the bytes
+//     are 0/1, so the products cannot carry into the nibble);
+//   * x-runs |dx| <= w: funnel shifts against the neighbouring words (lane
+//     shuffles; the segment-edge lanes load theirs; row ends replicate the
+//     edge voxel = the clamp), H_w = OP(H_{w-1}, x-w, x+w);
+//   * every (dz, dy) row of the SE is one AND/OR of H_{hw(dz,dy)} into the
+//     accumulator of its output slice: A[j] collects output (s - 2R + j) from
+//     input slice s, A[0] is complete after s and leaves unpacked
+//     ((nibble * 0x204081) & 0x01010101) as 2 x STG.128.
+// ~3 logic/pack instructions per voxel: the kernel is bound by HBM (1 B in,
+// 1 B out per voxel), not by the ALU.  Gated on the device grey check like
+// the byte-wise AND/OR kernel it replaces (nx % 32 == 0).
+// ---------------------------------------------------------------------------
+constexpr int MB_TY = HB_MB_TY, MB_WARPS = 8;
+
+__device__ __forceinline__ uint32_t mb_pack(const uint4& a, const uint4& b) {
+  const uint32_t c = 0x204081u;
+  const uint32_t b0 = (((a.x * c) >> 21) & 0x0Fu) | (((a.y * c) >> 17) & 0xF0u);
+  const uint32_t b1 = (((a.z * c) >> 21) & 0x0Fu) | (((a.w * c) >> 17) & 0xF0u);
+  const uint32_t b2 = (((b.x * c) >> 21) & 0x0Fu) | (((b.y * c) >> 17) & 0xF0u);
+  const uint32_t b3 = (((b.z * c) >> 21) & 0x0Fu) | (((b.w * c) >> 17) & 0xF0u);
+  return __byte_perm(__byte_perm(b0, b1, 0x0040), __byte_perm(b2, b3, 0x0040), 0x5410);
+}
+__device__ __forceinline__ void mb_unpack(uint32_t w, uint4& a, uint4& b) {
+  const uint32_t c = 0x204081u, m = 0x01010101u;
+  a.x = ((w & 0xFu) * c) & m;
+  a.y = (((w >> 4) & 0xFu) * c) & m;
+  a.z = (((w >> 8) & 0xFu) * c) & m;
+  a.w = (((w >> 12) & 0xFu) * c) & m;
+  b.x = (((w >> 16) & 0xFu) * c) & m;
+  b.y = (((w >> 20) & 0xFu) * c) & m;
+  b.z = (((w >> 24) & 0xFu) * c) & m;
+  b.w = ((w >> 28) * c) & m;
+}
+// packs 32 bytes; `grey` collects any bit a {0,1} byte cannot have
+__device__ __forceinline__ uint32_t mb_word(const uint8_t* p, uint32_t& grey) {
+  const uint4 a = __ldg(reinterpret_cast<const uint4*>(p));
+  const uint4 b = __ldg(reinterpret_cast<const uint4*>(p) + 1);
+  grey |= (a.x | a.y | a.z | a.w | b.x | b.y | b.z | b.w);
+  return mb_pack(a, b);
+}
+
+template <bool MAX, int KIND, int R>
+__global__ void __launch_bounds__(MB_WARPS * 32, 2)
+k_morph_bits(const uint8_t* __restrict__ in, int nz, int ny, int nx, int zo, int nzo, int zchunk,
+             uint8_t* __restrict__ out, int* __restrict__ grey_flag) {
+  using S = SeShape<KIND, R>;
+  constexpr int L = MB_TY + 2 * R;            // staged rows per thread
+  constexpr uint32_t ID = MAX ? 0u : ~0u;     // identity of the fold
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nw = nx >> 5;                     // words per row
+  const int wc = blockIdx.x * 32 + lane;      // this lane's word column
+  const bool active = wc < nw;
+  const int wcl = min(wc, nw - 1);
+  const int y0 = (blockIdx.y * MB_WARPS + warp) * MB_TY;
+  const int zs = blockIdx.z * zchunk, ze = min(zs + zchunk, nzo);
+  const int nsl = ze - zs + 2 * R;
+  const int64_t plane = (int64_t)ny * nx;
+  int64_t roff[L];
+#pragma unroll
+  for (int r = 0; r < L; ++r) roff[r] = (int64_t)min(max(y0 - R + r, 0), ny - 1) * nx;
+  uint32_t A[2 * R + 1][MB_TY];
+#pragma unroll
+  for (int j = 0; j < 2 * R + 1; ++j)
+#pragma unroll
+    for (int t = 0; t < MB_TY; ++t) A[j][t] = ID;
+  uint32_t grey = 0;
+  for (int s = 0; s < nsl; ++s) {
+    const int zi = min(max(zo + zs - R + s, 0), nz - 1);
+    const uint8_t* sl = in + (int64_t)zi * plane + (int64_t)wcl * 32;
+#pragma unroll
+    for (int r = 0; r < L; ++r) {
+      const uint8_t* rp = sl + roff[r];
+      const uint32_t p = mb_word(rp, grey);
+      uint32_t prv = __shfl_up_sync(0xffffffffu, p, 1);
+      uint32_t nxt = __shfl_down_sync(0xffffffffu, p, 1);
+      if (lane == 0) prv = wc == 0 ? 0u - (p & 1u) : mb_word(rp - 32, grey);
+      if (wc == nw - 1) nxt = 0u - (p >> 31);
+      else if (lane == 31) nxt = mb_word(rp + 32, grey);
+      uint32_t h[R + 1];
+      h[0] = p;
+#pragma unroll
+      for (int w = 1; w <= R; ++w) {
+        const uint32_t lo = __funnelshift_l(prv, p, w), hi = __funnelshift_r(p, nxt, w);
+        h[w] = MAX ? (h[w - 1] | lo | hi) : (h[w - 1] & lo & hi);
+      }
+#pragma unroll
+      for (int t = 0; t < MB_TY; ++t) {
+        const int dy = r - R - t;
+        if (dy < -R || dy > R) continue;
+#pragma unroll
+        for (int j = 0; j < 2 * R + 1; ++j) {
+          const int w = S::hw(R - j, dy);
+          if (w >= 0) A[j][t] = MAX ? (A[j][t] | h[w]) : (A[j][t] & h[w]);
+        }
+      }
+    }
+    const int o = s - 2 * R;  // output slice completed by this input slice
+    if (o >= 0 && active) {
+      uint8_t* op = out + (int64_t)(zs + o) * plane + (int64_t)wc * 32;
+#pragma unroll
+      for (int t = 0; t < MB_TY; ++t)
+        if (y0 + t < ny) {
+          uint4 a, b;
+          mb_unpack(A[0][t], a, b);
+          uint4* q = reinterpret_cast<uint4*>(op + (int64_t)(y0 + t) * nx);
+          q[0] = a;
+          q[1] = b;
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < 2 * R; ++j)
+#pragma unroll
+      for (int t = 0; t < MB_TY; ++t) A[j][t] = A[j + 1][t];
+#pragma unroll
+    for (int t = 0; t < MB_TY; ++t) A[2 * R][t] = ID;
+  }
+  // a byte > 1 anywhere in what this CTA read: the block is grey, this
+  // output is void and the u16-lane kernel queued behind rewrites it
+  if (__syncthreads_or((grey & 0xfefefefeu) != 0u) && threadIdx.x == 0) atomicOr(grey_flag, 1);
+}
+
+template <bool MAX, int KIND, int R>
+cudaError_t launch_morph_bits(const DevIn& in, int64_t zo, int64_t nzo, void* out, int* gate,
+                              cudaStream_t s) {
+  if (in.nx % 32 != 0 || (reinterpret_cast<uintptr_t>(in.p) & 15) != 0 ||
+      (reinterpret_cast<uintptr_t>(out) & 15) != 0 || in.nz >= (1 << 30) || in.ny >= (1 << 30) ||
+      in.nx >= (1 << 30) || std::getenv("HB_MORPH_NOBITS"))
+    return cudaErrorNotSupported;
+  const int nw = (int)(in.nx / 32);
+  dim3 grid((unsigned)((nw + 31) / 32), (unsigned)((in.ny + MB_WARPS * MB_TY - 1) / (MB_WARPS * MB_TY)), 1);
+  const int64_t tiles = (int64_t)grid.x * grid.y, slots = 2 * (int64_t)kNumSMs;
+  int zchunk = (int)std::min<int64_t>(nzo, 32);
+  double best = 1e300;
+  for (int64_t zc = std::max<int64_t>(32, nzo / 128); zc <= std::max<int64_t>(32, nzo); zc += 16) {
+    const int64_t ctas = tiles * ((nzo + zc - 1) / zc);
+    const double cost = (double)((ctas + slots - 1) / slots) * (double)(zc + 2 * R);
+    if (cost < best * 0.995) {
+      best = cost;
+      zchunk = (int)zc;
+    }
+  }
+  grid.z = (unsigned)((nzo + zchunk - 1) / zchunk);
+  k_morph_bits<MAX, KIND, R><<<grid, MB_WARPS * 32, 0, s>>>(
+      (const uint8_t*)in.p, (int)in.nz, (int)in.ny, (int)in.nx, (int)zo, (int)nzo, zchunk, (uint8_t*)out, gate);
+  return cudaGetLastError();
+}
+
 __global__ void k_u8_grey_check(const uint8_t* __restrict__ p, int64_t n, int* __restrict__ grey) {
   const int64_t n16 = n / 16;
   bool any = false;
@@ -887,6 +1044,17 @@ cudaError_t launch_morph3(const DevIn& in, int64_t zo, int64_t nzo, void* out, c
     cudaError_t e = cudaMallocAsync(&gate, sizeof(int), s);
     if (e != cudaSuccess) return e;
     cudaMemsetAsync(gate, 0, sizeof(int), s);
+    // whole-word rows: the one-bit-per-voxel kernel runs first and flags a
+    // grey block itself (no separate read pass); the u16-lane kernel behind
+    // it exits unless flagged
+    e = launch_morph_bits<MAX, KIND, R>(in, zo, nzo, out, gate, s);
+    if (e == cudaSuccess) {
+      e = launch_morph3_v<T, MAX, KIND, R, false>(in, zo, nzo, out, gate, s);
+      cudaFreeAsync(gate, s);
+      return e;
+    }
+    cudaGetLastError();
+    // else: device grey check gating the byte-wise AND/OR and the grey kernel
     k_u8_grey_check<<<kNumSMs * 4, 256, 0, s>>>((const uint8_t*)in.p, in.nz * in.ny * in.nx, gate);
     e = launch_morph3_v<T, MAX, KIND, R, true>(in, zo, nzo, out, gate, s);
     if (e == cudaSuccess) e = launch_morph3_v<T, MAX, KIND, R, false>(in, zo, nzo, out, gate, s);
