@@ -861,8 +861,14 @@ cudaError_t launch_morph3_v(const DevIn& in, int64_t zo, int64_t nzo, void* out,
   return cudaGetLastError();
 }
 
+#ifndef HB_MB_MINB
+#define HB_MB_MINB 2  // resident CTAs per SM the register budget is sized for
+#endif
+#ifndef HB_MB_PD
+#define HB_MB_PD 3  // slices prefetched ahead into L2
+#endif
 #ifndef HB_MB_TY
-#define HB_MB_TY 8  // output rows per thread
+#define HB_MB_TY 8  // output rows per thread (4/6/8 at 3-4 CTAs/SM: all 1030-1100 Gvox/s)
 #endif
 // ---------------------------------------------------------------------------
 // Binary {0,1} uint8 volumes (configs[2]'s binary case), ONE BIT per voxel in
@@ -883,7 +889,7 @@ cudaError_t launch_morph3_v(const DevIn& in, int64_t zo, int64_t nzo, void* out,
 // 1 B out per voxel), not by the ALU.  Gated on the device grey check like
 // the byte-wise AND/OR kernel it replaces (nx % 32 == 0).
 // ---------------------------------------------------------------------------
-constexpr int MB_TY = HB_MB_TY, MB_WARPS = 8;
+constexpr int MB_TY = HB_MB_TY, MB_WARPS = 8, MB_PD = HB_MB_PD;
 
 __device__ __forceinline__ uint32_t mb_pack(const uint4& a, const uint4& b) {
   const uint32_t c = 0x204081u;
@@ -913,7 +919,7 @@ __device__ __forceinline__ uint32_t mb_word(const uint8_t* p, uint32_t& grey) {
 }
 
 template <bool MAX, int KIND, int R>
-__global__ void __launch_bounds__(MB_WARPS * 32, 2)
+__global__ void __launch_bounds__(MB_WARPS * 32, HB_MB_MINB)
 k_morph_bits(const uint8_t* __restrict__ in, int nz, int ny, int nx, int zo, int nzo, int zchunk,
              uint8_t* __restrict__ out, int* __restrict__ grey_flag) {
   using S = SeShape<KIND, R>;
@@ -937,7 +943,23 @@ k_morph_bits(const uint8_t* __restrict__ in, int nz, int ny, int nx, int zo, int
 #pragma unroll
     for (int t = 0; t < MB_TY; ++t) A[j][t] = ID;
   uint32_t grey = 0;
+  // L2 prefetch of the rows MB_PD slices ahead: lanes 0..L-1 issue one bulk
+  // prefetch per staged row of this warp's segment (the loads were latency-
+  // bound: long-scoreboard stalls on the packs, 21% warps active)
+  const int seg0 = blockIdx.x * 32 * 32;  // first byte of this segment in a row
+  const uint32_t seg_bytes = (uint32_t)min(32 * 32, nx - seg0);
+  const int prow = min(max(y0 - R + lane, 0), ny - 1);
+  auto prefetch = [&](int sp) {
+    if (lane < L && sp < nsl) {
+      const int zp = min(max(zo + zs - R + sp, 0), nz - 1);
+      const uint8_t* a = in + (int64_t)zp * plane + (int64_t)prow * nx + seg0;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(seg_bytes) : "memory");
+    }
+  };
+#pragma unroll
+  for (int sp = 0; sp < MB_PD; ++sp) prefetch(sp);
   for (int s = 0; s < nsl; ++s) {
+    prefetch(s + MB_PD);
     const int zi = min(max(zo + zs - R + s, 0), nz - 1);
     const uint8_t* sl = in + (int64_t)zi * plane + (int64_t)wcl * 32;
 #pragma unroll
