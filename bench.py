@@ -253,6 +253,42 @@ def cpu_baseline_and_parity(x, out_g, out_m, yx):
     return cpu, parity
 
 
+def reference_python_sample(yx):
+    """The reference itself (harpia, pure Python over scipy, installed offline
+    into baseline/_ref) on ONE core: gaussian sigma=2 on 8 output slices and
+    median r=1 on 2 output slices of a yx^2 f32 slab, through its own
+    registry.run_operator (single chunk).  None when baseline/_ref is absent.
+    Reported beside the port; the port stays the arm's value."""
+    ref_root = ROOT / "baseline" / "_ref"
+    if not (ref_root / "harpia").is_dir():
+        return None
+    try:
+        if str(ref_root) not in sys.path:
+            sys.path.insert(0, str(ref_root))
+        from harpia import registry as hreg
+        from harpia.chunking import MemoryBudget as HBudget
+
+        big = HBudget(1 << 40, 1.0)
+        rng = np.random.default_rng(5)
+        xg = rng.random((8 + 2 * HALO_G, yx, yx), dtype=np.float32)
+        xm = rng.random((2 + 2, yx, yx), dtype=np.float32)
+        t0 = time.perf_counter()
+        hreg.run_operator(xg, "gaussian", {"sigma": 2.0}, big)
+        tg = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        hreg.run_operator(xm, "median", {"radius": 1}, big)
+        tm = time.perf_counter() - t0
+        vg, vm = xg.size, xm.size  # the reference filters the whole slab it is given
+        return {"value": round(2.0 / (tg / vg + tm / vm) / 1e9, 6), "unit": UNIT, "cores": 1,
+                "kind": "reference",
+                "sample": f"harpia.registry.run_operator (baseline/_ref, 1 thread): gaussian "
+                          f"sigma=2 on a {xg.shape[0]}x{yx}^2 slab, median r=1 on a "
+                          f"{xm.shape[0]}x{yx}^2 slab, single chunk",
+                "gaussian_mvox_s": round(vg / tg / 1e6, 3), "median_mvox_s": round(vm / tm / 1e6, 3)}
+    except Exception as exc:  # the extra field must never break the bench
+        return {"error": f"{type(exc).__name__}: {exc}"[:200]}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -285,6 +321,9 @@ def run_reference(args):
         "e2e": {"value": round(value, 6), "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
+    rp = reference_python_sample(yx)
+    if rp is not None:
+        line["reference_python"] = rp
     print(json.dumps(line), flush=True)
     return 0
 
@@ -368,6 +407,9 @@ def run_ours(args):
     cpu = parity = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu, parity = cpu_baseline_and_parity(x, out_g, out_m, n)
+        rp = reference_python_sample(n)
+        if rp is not None:
+            cpu["reference_python"] = rp
     del x, out_g, out_m
     torch.cuda.synchronize()
     filters_out.update(side_filters(n, peak, stream))
