@@ -112,11 +112,16 @@ __device__ __forceinline__ void clamp_stage(float* st, int pitch, int h, int w, 
 #ifndef HB_GTRI_NST
 #define HB_GTRI_NST 10
 #endif
-constexpr int TX = 48, TY = 32;
+#ifndef HB_GTRI_TY
+#define HB_GTRI_TY 32  // 32: one 640-thread CTA/SM with setmaxnreg; 16: two 320-thread CTAs/SM (measured 265 vs 310 Gvox/s)
+#endif
+constexpr int TX = 48, TY = HB_GTRI_TY;
+constexpr int CTAS_PER_SM = TY == 32 ? 1 : 2;
+constexpr bool kSetMaxNreg = TY == 32;  // role warp counts are whole warpgroups only at TY = 32
 constexpr int YR = 8;   // rows per Y item
 constexpr int XC = 6;   // columns per X item
-constexpr int NYT = 128, NXT = 128, NZT = (TX / 2) * (TY / 2);  // 4 + 4 + 12 warps
-constexpr int NT = NYT + NXT + NZT;                              // 640
+constexpr int NYT = 4 * TY, NXT = 4 * TY, NZT = (TX / 2) * (TY / 2);  // 4 + 4 + 12 warps at TY = 32
+constexpr int NT = NYT + NXT + NZT;                                    // 640 at TY = 32
 // setmaxnreg (warpgroup-wide; an .inc draws only on what this CTA's .dec
 // released): launch at 96, Y -> 56 and X -> 80 free 5120 + 2048 registers,
 // the Z warps take 384 x 16 of them
@@ -165,7 +170,7 @@ struct GeoT {
 };
 
 template <int R, bool UNSHARP>
-__global__ void __launch_bounds__(NT, 1)
+__global__ void __launch_bounds__(NT, CTAS_PER_SM)
 k_gauss_tri(const __grid_constant__ CUtensorMap tin, const float* __restrict__ orig,
             float* __restrict__ out, const __grid_constant__ TriArgs a) {
   using G = GeoT<R>;
@@ -205,7 +210,7 @@ k_gauss_tri(const __grid_constant__ CUtensorMap tin, const float* __restrict__ o
 
   if (tid >= NZT + NXT) {
     // =================== Y role: TMA producer + y pass ======================
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kYRegs));
+    if constexpr (kSetMaxNreg) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kYRegs));
     const int yt = tid - (NZT + NXT);
     auto zin_of = [&](int s) { return min(max(a.zo + z0 - R + s, 0), a.nzi - 1); };
     const bool border =
@@ -271,7 +276,7 @@ k_gauss_tri(const __grid_constant__ CUtensorMap tin, const float* __restrict__ o
 
   if (tid >= NZT) {
     // ========================= X role: x pass ================================
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kXRegs));
+    if constexpr (kSetMaxNreg) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kXRegs));
     const int xt = tid - NZT;
     const int rp = xt / (TX / XC), g = xt % (TX / XC);
     const float* const srow = sY + rp * G::SYP + 2 * XC * g;  // pair (XC*g) of row pair rp
@@ -324,7 +329,7 @@ k_gauss_tri(const __grid_constant__ CUtensorMap tin, const float* __restrict__ o
   }
 
   // ======================== Z role: ring, z pass, store ======================
-  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kZRegs));
+  if constexpr (kSetMaxNreg) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kZRegs));
   const int cp = tid % (TX / 2), rp = tid / (TX / 2);
   const int gy = y0 + 2 * rp, gx = x0 + 2 * cp;
   const bool live_c = gx < a.nx;  // nx even: both columns in or out
@@ -438,7 +443,7 @@ cudaError_t launch_tri(const DevIn& in, int64_t zo, int64_t nzo, float* out, con
   const char* zv = std::getenv("HB_G3_ZCAP");
   const int zcap = zv ? std::max(16, std::atoi(zv)) : 192;
   const int64_t tiles = (int64_t)gx * gy;
-  const int64_t slots = kNumSMs;
+  const int64_t slots = (int64_t)kNumSMs * CTAS_PER_SM;
   double best = 1e300;
   int64_t best_split = 1;
   const int64_t min_split = std::max<int64_t>(1, (nzo + zcap - 1) / zcap);
