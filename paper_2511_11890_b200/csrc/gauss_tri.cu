@@ -72,9 +72,21 @@ __device__ __forceinline__ void arrive(uint64_t* bar) {
 // one arrival per warp (barrier counts are in warps): per-thread arrivals on
 // the same mbarrier serialise in the LSU — 768 of them per slice cost about
 // as long as the slice's arithmetic
+// HB_GTRI_THREAD_ARRIVE=1 builds the per-thread form (barrier counts in
+// threads) — compute-sanitizer racecheck does not model the elected-lane
+// release through __syncwarp and reports the sX/sY reuse as hazards; the
+// per-thread build is the one it checks (0 hazards, profiles/r02_sanitizer.md)
+#ifndef HB_GTRI_THREAD_ARRIVE
+#define HB_GTRI_THREAD_ARRIVE 0
+#endif
+constexpr int kArrivePerWarp = HB_GTRI_THREAD_ARRIVE ? 32 : 1;
 __device__ __forceinline__ void warp_arrive(uint64_t* bar) {
+#if HB_GTRI_THREAD_ARRIVE
+  arrive(bar);
+#else
   __syncwarp();
   if ((threadIdx.x & 31) == 0) arrive(bar);
+#endif
 }
 __device__ __forceinline__ void named_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
@@ -196,13 +208,13 @@ k_gauss_tri(const __grid_constant__ CUtensorMap tin, const float* __restrict__ o
     for (int i = 0; i < G::NST; ++i) mbar_init(&bar_tma[i], 1);
 #pragma unroll
     for (int i = 0; i < G::NSY; ++i) {
-      mbar_init(&full_y[i], NYT / 32);
-      mbar_init(&empty_y[i], NXT / 32);
+      mbar_init(&full_y[i], NYT / 32 * kArrivePerWarp);
+      mbar_init(&empty_y[i], NXT / 32 * kArrivePerWarp);
     }
 #pragma unroll
     for (int i = 0; i < G::NSX; ++i) {
-      mbar_init(&full_x[i], NXT / 32);
-      mbar_init(&empty_x[i], NZT / 32);
+      mbar_init(&full_x[i], NXT / 32 * kArrivePerWarp);
+      mbar_init(&empty_x[i], NZT / 32 * kArrivePerWarp);
     }
     fence_mbar_init();
   }

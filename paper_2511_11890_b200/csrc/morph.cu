@@ -970,7 +970,7 @@ k_morph_bits(const uint8_t* __restrict__ in, int nz, int ny, int nx, int zo, int
       uint32_t nxt = __shfl_down_sync(0xffffffffu, p, 1);
       if (lane == 0) prv = wc == 0 ? 0u - (p & 1u) : mb_word(rp - 32, grey);
       if (wc == nw - 1) nxt = 0u - (p >> 31);
-      else if (lane == 31) nxt = mb_word(rp + 32, grey);
+      else if (lane == 31 && wc + 1 < nw) nxt = mb_word(rp + 32, grey);  // lanes past the row end are idle
       uint32_t h[R + 1];
       h[0] = p;
 #pragma unroll
