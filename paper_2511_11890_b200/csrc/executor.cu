@@ -7,6 +7,7 @@
 // synchronous job the pool is trimmed to zero, so the job's device residual is
 // exactly 0 and PyTorch's caching allocator is never involved.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges for ncu --nvtx / nsys (no-ops without a tool)
 
 #include <algorithm>
 #include <atomic>
@@ -25,6 +26,14 @@
 #include "ops.cuh"
 
 using namespace hb;
+
+namespace {
+// NVTX range (job / chunk-piece / device-apply) on the calling host thread
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
 
 namespace {
 
@@ -1425,6 +1434,7 @@ int64_t hb_device_pool_bytes(int32_t dev) {
 int32_t hb_apply_device(const hb_volume* in, hb_volume* out, const hb_stage* stages,
                         int32_t nstages, int64_t z_begin, void* stream, int32_t synchronize,
                         hb_report* rep) {
+  NvtxRange nv_range("hb_apply_device");
   if (rep) {
     std::memset(rep, 0, sizeof(*rep));
     rep->failed_chunk = -1;
@@ -1680,6 +1690,7 @@ static int32_t run_host_range(const hb_volume* in, hb_volume* out,
   auto finish = [&](int64_t j) -> cudaError_t {
     const int slot = (int)(j % depth);
     const Piece& pc = pieces[j];
+    NvtxRange fin_range("hb piece finish (D2H)");
     const size_t bytes = (size_t)(pc.b - pc.a) * plane * out_es;
     char* host_dst = (char*)out->data + (size_t)pc.a * plane * out_es;
     cudaError_t err = cudaSuccess;
@@ -1703,6 +1714,9 @@ static int32_t run_host_range(const hb_volume* in, hb_volume* out,
   for (; j < npieces; j++) {
     const Piece& pc = pieces[j];
     const int slot = (int)(j % depth);
+    char nv[48];
+    std::snprintf(nv, sizeof(nv), "hb chunk %lld piece %lld", (long long)pc.chunk, (long long)j);
+    NvtxRange piece_range(nv);  // host-side enqueue of H2D -> chain -> D2H
     if (pc.chunk != chunk_now) {  // chunk boundary: cancel poll + fault hook
       chunk_now = pc.chunk;
       if (ex->cancel && ex->cancel(ex->cancel_ctx)) {
@@ -1839,6 +1853,7 @@ int32_t hb_run(const hb_volume* in, hb_volume* out, const hb_stage* stages, int3
   std::vector<StageDesc> st;
   int32_t rc = check_run(in, out, stages, nstages, chunks, nchunks, ex, rep, st);
   if (rc != HB_OK) return rc;
+  NvtxRange job("hb_run");
   return run_host_range(in, out, st, chunks, nchunks, ex, rep, t_start);
 }
 
