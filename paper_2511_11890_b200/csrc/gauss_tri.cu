@@ -145,7 +145,6 @@ struct TriArgs {
   f2 w2[17];  // (w_k, w_k): FFMA2 operands
   int nzi, zo, nzo, zchunk, nx, ny;
   float amount;
-  int dbg;  // A/B only: bit0/1/2 skip the y/x/z arithmetic (wrong results)
 };
 
 template <int R>
@@ -251,7 +250,7 @@ k_gauss_tri(const __grid_constant__ CUtensorMap tin, const float* __restrict__ o
         named_sync(1, NYT);
       }
       if (s >= G::NSY) mbar_wait(&empty_y[b], ph_e);
-      if (active && !(a.dbg & 1)) {
+      if (active) {
         f2 acc[YR];
         const float* src = stage + src_off;
 #pragma unroll
@@ -307,10 +306,6 @@ k_gauss_tri(const __grid_constant__ CUtensorMap tin, const float* __restrict__ o
       }
       // symmetric fold per output column j (taps v[j .. j + 2R]), two chains
       f2 o[XC];
-      if (a.dbg & 2) {
-#pragma unroll
-        for (int j = 0; j < XC; ++j) o[j] = v[j];
-      } else
 #pragma unroll
       for (int j = 0; j < XC; ++j) {
         f2 e = mul2(v[j + R], a.w2[R]);
@@ -372,10 +367,6 @@ k_gauss_tri(const __grid_constant__ CUtensorMap tin, const float* __restrict__ o
       if (o >= 0) {
         // slices o .. o + 2R live in ring slots (u + k) % RING, k = 0 .. 2R
         f2 zr[2];
-        if (a.dbg & 4) {
-          zr[0] = ring[u][0];
-          zr[1] = ring[u][1];
-        } else
 #pragma unroll
         for (int m = 0; m < 2; ++m) {
           f2 e = mul2(ring[(u + R) % G::RING][m], a.w2[R]);
@@ -443,8 +434,6 @@ cudaError_t launch_tri(const DevIn& in, int64_t zo, int64_t nzo, float* out, con
   a.nx = (int)in.nx;
   a.ny = (int)in.ny;
   a.amount = epi.amount;
-  const char* dv = std::getenv("HB_GTRI_DBG");
-  a.dbg = dv ? std::atoi(dv) : 0;
   auto kern = k_gauss_tri<R, UNSHARP>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM) != cudaSuccess)
     return cudaErrorNotSupported;
