@@ -514,8 +514,17 @@ cudaError_t run_stage_impl(const StageDesc& d, const DevIn& in, int64_t zo, int6
       return median(in, zo, nzo, out, d.radius, s, launches);
     case HB_OP_ERODE:
     case HB_OP_DILATE:
+    {
+      // the u8 binary/grey gate word comes from the job's pool (a per-call
+      // stream-ordered allocation measured noisy: +/-30% on 2 ms launches)
+      int* gate = in.dt == HB_U8 ? (int*)pa.get(256) : nullptr;
+      if (in.dt == HB_U8 && !gate) {  // no room: morph() allocates its own word
+        pa.err = cudaSuccess;
+        cudaGetLastError();
+      }
       return morph(in, zo, nzo, out, d.offsets.data(), (int)(d.offsets.size() / 3),
-                   d.op == HB_OP_DILATE, s, launches);
+                   d.op == HB_OP_DILATE, s, launches, gate);
+    }
   }
   return cudaErrorInvalidValue;
 }

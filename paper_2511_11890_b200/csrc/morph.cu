@@ -1014,6 +1014,197 @@ k_morph_bits(const uint8_t* __restrict__ in, int nz, int ny, int nx, int zo, int
   if (__syncthreads_or((grey & 0xfefefefeu) != 0u) && threadIdx.x == 0) atomicOr(grey_flag, 1);
 }
 
+// ---------------------------------------------------------------------------
+// k_morph_bits2: the same one-bit-per-voxel erosion / dilation with the input
+// staged by TMA (k_morph_bits above was load-latency-bound: each thread
+// loaded and packed its 8 + 2R rows itself, long-scoreboard 67%).  CTA tile =
+// 64 output rows x 8 words (256 voxels); per slice two TMA boxes (160 B x
+// (64 + 2R) rows: the 256 columns plus one halo word each side) land in a
+// 3-deep ring; every staged row word is packed ONCE into a shared bit plane
+// (double-buffered), then a thread (one word x 2 output rows) builds its
+// x-runs from the packed words of its 2 + 2R rows and folds the SE rows into
+// per-output-slice accumulators exactly as k_morph_bits does.  Border tiles
+// replicate the edge bytes (the clamp) before packing.
+// ---------------------------------------------------------------------------
+constexpr int MB2_TXW = 8, MB2_TYO = 64, MB2_NT = 256, MB2_NST = 3;
+constexpr int MB2_BOXW = 160;  // bytes per TMA box row (half of 32 + 256 + 32)
+
+template <int R>
+struct MB2Geo {
+  static constexpr int ROWS = MB2_TYO + 2 * R;
+  static constexpr int BOX = MB2_BOXW * ROWS;              // bytes per box
+  static constexpr int BOXP = (BOX + 127) / 128 * 128;     // TMA destinations are 128-B aligned
+  static constexpr int STAGE = 2 * BOXP;
+  static constexpr int PW = MB2_TXW + 2;                    // packed words per row (1 halo each side)
+  static constexpr int PLANE = ROWS * PW;                   // packed words per slice
+  static constexpr int OFF_P = MB2_NST * STAGE;
+  static constexpr int OFF_BAR = OFF_P + 2 * PLANE * 4;
+  static constexpr int SMEM = OFF_BAR + MB2_NST * 8 + 128;
+};
+
+template <bool MAX, int KIND, int R>
+__global__ void __launch_bounds__(MB2_NT, 2)
+k_morph_bits2(const __grid_constant__ CUtensorMap tin, uint8_t* __restrict__ out, int nz, int ny,
+              int nx, int zo, int nzo, int zchunk, int* __restrict__ grey_flag) {
+  using S = SeShape<KIND, R>;
+  using G = MB2Geo<R>;
+  constexpr uint32_t ID = MAX ? 0u : ~0u;
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
+  uint32_t* sP = reinterpret_cast<uint32_t*>(smem + G::OFF_P);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + G::OFF_BAR);
+  const int tid = threadIdx.x;
+  const int x0 = blockIdx.x * (MB2_TXW * 32), y0 = blockIdx.y * MB2_TYO;
+  const int zs = blockIdx.z * zchunk, ze = min(zs + zchunk, nzo);
+  const int nsl = ze - zs + 2 * R;
+  auto zin = [&](int k) { return min(max(zo + zs - R + k, 0), nz - 1); };
+  auto load = [&](int k, int stg) {
+    unsigned char* d = smem + stg * G::STAGE;
+    mbar_expect_tx(&bar[stg], 2 * G::BOX);
+    tma_load_3d(d, &tin, x0 - 32, y0 - R, zin(k), &bar[stg]);
+    tma_load_3d(d + G::BOXP, &tin, x0 - 32 + MB2_BOXW, y0 - R, zin(k), &bar[stg]);
+  };
+  if (tid == 0) {
+#pragma unroll
+    for (int i = 0; i < MB2_NST; ++i) mbar_init(&bar[i], 1);
+    fence_mbar_init();
+    prefetch_tmap(&tin);
+    for (int i = 0; i < MB2_NST && i < nsl; ++i) load(i, i);
+  }
+  __syncthreads();
+  const bool border = x0 - 32 < 0 || x0 + MB2_TXW * 32 + 32 > nx || y0 - R < 0 || y0 + MB2_TYO + R > ny;
+  // this thread: word w of the tile, output rows y0 + 2g, y0 + 2g + 1
+  const int w = tid % MB2_TXW, g = tid / MB2_TXW;
+  const int gw = (x0 >> 5) + w;  // global word column
+  const bool active = gw < (nx >> 5);
+  const int64_t plane = (int64_t)ny * nx;
+  uint32_t A[2 * R + 1][2];
+#pragma unroll
+  for (int j = 0; j < 2 * R + 1; ++j) A[j][0] = A[j][1] = ID;
+  uint32_t grey = 0;
+  int st = 0;
+  uint32_t ph = 0;
+  for (int s = 0; s < nsl; ++s) {
+    unsigned char* stage = smem + st * G::STAGE;
+    mbar_wait(&bar[st], ph);
+    // pack every staged row word once (buffer s & 1)
+    uint32_t* P = sP + (s & 1) * G::PLANE;
+    for (int e = tid; e < G::PLANE; e += MB2_NT) {
+      const int r = e / G::PW, c = e - r * G::PW;  // c: word 0..9 of the staged row
+      const unsigned char* src = stage + (c < 5 ? 0 : G::BOXP) + r * MB2_BOXW + (c % 5) * 32;
+      const uint4 a = *reinterpret_cast<const uint4*>(src);
+      const uint4 b = *reinterpret_cast<const uint4*>(src + 16);
+      grey |= (a.x | a.y | a.z | a.w | b.x | b.y | b.z | b.w);
+      P[e] = mb_pack(a, b);
+    }
+    __syncthreads();  // P complete; stage st fully read
+    if (border) {
+      // clamp-to-edge in the bit domain (TMA zero-filled the out-of-volume
+      // bytes): halo words beyond a row end take the edge voxel's bit, then
+      // rows beyond the volume copy the nearest valid row
+      const int r_lo = max(0, -(y0 - R)), r_hi = min(G::ROWS, ny - (y0 - R));
+      const int w_lo = max(0, -((x0 >> 5) - 1)), w_hi = min(G::PW, (nx >> 5) - ((x0 >> 5) - 1));
+      if (tid < G::ROWS && tid >= r_lo && tid < r_hi) {
+        uint32_t* row = P + tid * G::PW;
+        const uint32_t left = 0u - (row[w_lo] & 1u), right = 0u - (row[w_hi - 1] >> 31);
+        for (int c = 0; c < w_lo; ++c) row[c] = left;
+        for (int c = w_hi; c < G::PW; ++c) row[c] = right;
+      }
+      __syncthreads();
+      for (int e = tid; e < G::PLANE; e += MB2_NT) {
+        const int r = e / G::PW, c = e - r * G::PW;
+        if (r < r_lo || r >= r_hi) P[e] = P[min(max(r, r_lo), r_hi - 1) * G::PW + c];
+      }
+      __syncthreads();
+    }
+    if (tid == 0 && s + MB2_NST < nsl) {
+      fence_proxy_async();
+      load(s + MB2_NST, st);
+    }
+    if (++st == MB2_NST) { st = 0; ph ^= 1u; }
+    // x-runs of the 2 + 2R rows this thread needs, folded per SE row
+#pragma unroll
+    for (int r = 0; r < 2 + 2 * R; ++r) {
+      const uint32_t* row = P + (2 * g + r) * G::PW + w;  // words w-1, w, w+1 at +0, +1, +2
+      const uint32_t prv = row[0], p = row[1], nxt = row[2];
+      uint32_t h[R + 1];
+      h[0] = p;
+#pragma unroll
+      for (int k = 1; k <= R; ++k) {
+        const uint32_t lo = __funnelshift_l(prv, p, k), hi = __funnelshift_r(p, nxt, k);
+        h[k] = MAX ? (h[k - 1] | lo | hi) : (h[k - 1] & lo & hi);
+      }
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        const int dy = r - R - t;
+        if (dy < -R || dy > R) continue;
+#pragma unroll
+        for (int j = 0; j < 2 * R + 1; ++j) {
+          const int hw = S::hw(R - j, dy);
+          if (hw >= 0) A[j][t] = MAX ? (A[j][t] | h[hw]) : (A[j][t] & h[hw]);
+        }
+      }
+    }
+    const int o = s - 2 * R;
+    if (o >= 0 && active) {
+      uint8_t* op = out + (int64_t)(zs + o) * plane + (int64_t)gw * 32;
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        const int y = y0 + 2 * g + t;
+        if (y < ny) {
+          uint4 a, b;
+          mb_unpack(A[0][t], a, b);
+          uint4* q = reinterpret_cast<uint4*>(op + (int64_t)y * nx);
+          q[0] = a;
+          q[1] = b;
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 2 * R; ++j) A[j][0] = A[j + 1][0], A[j][1] = A[j + 1][1];
+    A[2 * R][0] = A[2 * R][1] = ID;
+  }
+  if (__syncthreads_or((grey & 0xfefefefeu) != 0u) && tid == 0) atomicOr(grey_flag, 1);
+}
+
+template <bool MAX, int KIND, int R>
+cudaError_t launch_morph_bits2(const DevIn& in, int64_t zo, int64_t nzo, void* out, int* gate,
+                               cudaStream_t s) {
+  using G = MB2Geo<R>;
+  if (in.nx % 32 != 0 || (reinterpret_cast<uintptr_t>(in.p) & 15) != 0 ||
+      (reinterpret_cast<uintptr_t>(out) & 15) != 0 || in.nz >= (1 << 30) || in.ny >= (1 << 30) ||
+      in.nx >= (1 << 30) || std::getenv("HB_MORPH_BITS1"))
+    return cudaErrorNotSupported;
+  CUtensorMap tin;
+  if (!make_tmap_3d(&tin, in.p, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, in.nx, in.ny, in.nz, MB2_BOXW, G::ROWS))
+    return cudaErrorNotSupported;
+  auto kern = k_morph_bits2<MAX, KIND, R>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM) != cudaSuccess)
+    return cudaErrorNotSupported;
+  dim3 grid((unsigned)((in.nx + MB2_TXW * 32 - 1) / (MB2_TXW * 32)),
+            (unsigned)((in.ny + MB2_TYO - 1) / MB2_TYO), 1);
+  const int64_t tiles = (int64_t)grid.x * grid.y, slots = 2 * (int64_t)kNumSMs;
+  // z-chunks capped (HB_MB2_ZCAP, default 48 slices; 32-48: 2645, 64-128: 2340 Gvox/s) so neighbouring tiles,
+  // which re-read each other's halo rows and words, stay close in z and hit
+  // in L2 (uncapped runs drifted apart: 1.41x DRAM reads)
+  const char* zv = std::getenv("HB_MB2_ZCAP");
+  const int64_t zcap = zv ? std::max(16, std::atoi(zv)) : 48;
+  int zchunk = (int)std::min<int64_t>(nzo, 16);
+  double best = 1e300;
+  for (int64_t zc = 16; zc <= std::max<int64_t>(16, std::min<int64_t>(nzo, zcap)); zc += 8) {
+    const int64_t ctas = tiles * ((nzo + zc - 1) / zc);
+    const double cost = (double)((ctas + slots - 1) / slots) * (double)(zc + 2 * R);
+    if (cost < best * 0.995) {
+      best = cost;
+      zchunk = (int)zc;
+    }
+  }
+  grid.z = (unsigned)((nzo + zchunk - 1) / zchunk);
+  kern<<<grid, MB2_NT, G::SMEM, s>>>(tin, (uint8_t*)out, (int)in.nz, (int)in.ny, (int)in.nx, (int)zo,
+                                      (int)nzo, zchunk, gate);
+  return cudaGetLastError();
+}
+
 template <bool MAX, int KIND, int R>
 cudaError_t launch_morph_bits(const DevIn& in, int64_t zo, int64_t nzo, void* out, int* gate,
                               cudaStream_t s) {
@@ -1056,23 +1247,34 @@ __global__ void k_u8_grey_check(const uint8_t* __restrict__ p, int64_t n, int* _
 // gates the binary (AND/OR, 4 voxels per op) and the grey kernel; both are
 // enqueued and the unselected one exits at once — no host round trip.
 template <typename T, bool MAX, int KIND, int R>
-cudaError_t launch_morph3(const DevIn& in, int64_t zo, int64_t nzo, void* out, cudaStream_t s) {
+cudaError_t launch_morph3(const DevIn& in, int64_t zo, int64_t nzo, void* out, cudaStream_t s,
+                          int* gate_scratch) {
   if constexpr (sizeof(T) == 2) {
     return launch_morph3_v<T, MAX, KIND, R, false>(in, zo, nzo, out, nullptr, s);
   } else {
     if ((reinterpret_cast<uintptr_t>(in.p) & 15) != 0 || std::getenv("HB_MORPH_NOBIN"))
       return launch_morph3_v<T, MAX, KIND, R, false>(in, zo, nzo, out, nullptr, s);
-    int* gate = nullptr;
-    cudaError_t e = cudaMallocAsync(&gate, sizeof(int), s);
-    if (e != cudaSuccess) return e;
+    int* gate = gate_scratch;
+    cudaError_t e = cudaSuccess;
+    if (!gate) {
+      e = cudaMallocAsync(&gate, sizeof(int), s);
+      if (e != cudaSuccess) return e;
+    }
     cudaMemsetAsync(gate, 0, sizeof(int), s);
+    auto release = [&]() {
+      if (!gate_scratch) cudaFreeAsync(gate, s);
+    };
     // whole-word rows: the one-bit-per-voxel kernel runs first and flags a
     // grey block itself (no separate read pass); the u16-lane kernel behind
     // it exits unless flagged
-    e = launch_morph_bits<MAX, KIND, R>(in, zo, nzo, out, gate, s);
+    e = launch_morph_bits2<MAX, KIND, R>(in, zo, nzo, out, gate, s);
+    if (e == cudaErrorNotSupported) {
+      cudaGetLastError();
+      e = launch_morph_bits<MAX, KIND, R>(in, zo, nzo, out, gate, s);
+    }
     if (e == cudaSuccess) {
       e = launch_morph3_v<T, MAX, KIND, R, false>(in, zo, nzo, out, gate, s);
-      cudaFreeAsync(gate, s);
+      release();
       return e;
     }
     cudaGetLastError();
@@ -1080,19 +1282,19 @@ cudaError_t launch_morph3(const DevIn& in, int64_t zo, int64_t nzo, void* out, c
     k_u8_grey_check<<<kNumSMs * 4, 256, 0, s>>>((const uint8_t*)in.p, in.nz * in.ny * in.nx, gate);
     e = launch_morph3_v<T, MAX, KIND, R, true>(in, zo, nzo, out, gate, s);
     if (e == cudaSuccess) e = launch_morph3_v<T, MAX, KIND, R, false>(in, zo, nzo, out, gate, s);
-    cudaFreeAsync(gate, s);
+    release();
     return e;
   }
 }
 
 template <typename T, bool MAX>
 cudaError_t dispatch_morph3(int kind, int r, const DevIn& in, int64_t zo, int64_t nzo, void* out,
-                            cudaStream_t s) {
+                            cudaStream_t s, int* gate = nullptr) {
 #define HB_M3_K(K)                                                              \
   if (kind == K) {                                                              \
-    if (r == 1) return launch_morph3<T, MAX, K, 1>(in, zo, nzo, out, s);        \
-    if (r == 2) return launch_morph3<T, MAX, K, 2>(in, zo, nzo, out, s);        \
-    if (r == 3) return launch_morph3<T, MAX, K, 3>(in, zo, nzo, out, s);        \
+    if (r == 1) return launch_morph3<T, MAX, K, 1>(in, zo, nzo, out, s, gate);  \
+    if (r == 2) return launch_morph3<T, MAX, K, 2>(in, zo, nzo, out, s, gate);  \
+    if (r == 3) return launch_morph3<T, MAX, K, 3>(in, zo, nzo, out, s, gate);  \
   }
   HB_M3_K(SE_BALL) HB_M3_K(SE_BOX) HB_M3_K(SE_CROSS)
 #undef HB_M3_K
@@ -1102,7 +1304,7 @@ cudaError_t dispatch_morph3(int kind, int r, const DevIn& in, int64_t zo, int64_
 }  // namespace
 
 cudaError_t morph(const DevIn& in, int64_t zo, int64_t nzo, void* out, const int32_t* offsets,
-                  int n, bool is_max, cudaStream_t s, int64_t* launches) {
+                  int n, bool is_max, cudaStream_t s, int64_t* launches, int* gate) {
   if (nzo <= 0) return cudaSuccess;
   if ((in.dt == HB_U16 || in.dt == HB_U8) && in.nx >= 8 && in.ny >= 8) {
     int kind = 0, rr = 0;
@@ -1112,8 +1314,8 @@ cudaError_t morph(const DevIn& in, int64_t zo, int64_t nzo, void* out, const int
         e = is_max ? dispatch_morph3<uint16_t, true>(kind, rr, in, zo, nzo, out, s)
                    : dispatch_morph3<uint16_t, false>(kind, rr, in, zo, nzo, out, s);
       else
-        e = is_max ? dispatch_morph3<uint8_t, true>(kind, rr, in, zo, nzo, out, s)
-                   : dispatch_morph3<uint8_t, false>(kind, rr, in, zo, nzo, out, s);
+        e = is_max ? dispatch_morph3<uint8_t, true>(kind, rr, in, zo, nzo, out, s, gate)
+                   : dispatch_morph3<uint8_t, false>(kind, rr, in, zo, nzo, out, s, gate);
       if (e != cudaErrorNotSupported) {
         if (e == cudaSuccess && launches) *launches += 1;
         return e;

@@ -158,8 +158,10 @@ cudaError_t median(const DevIn& in, int64_t zo, int64_t nzo, void* out, int r,
 // --- flat grey morphology (morph.cu) --------------------------------------
 // offsets: 3*n ints (dz,dy,dx) host array; is_max selects dilation, in which
 // case the caller has already reflected the SE (morphology.py:119-121).
+// `gate` (optional): a device int of scratch for the u8 binary/grey gate
+// (from the executor's pool); null -> a stream-ordered allocation per call.
 cudaError_t morph(const DevIn& in, int64_t zo, int64_t nzo, void* out,
                   const int32_t* offsets, int n, bool is_max, cudaStream_t s,
-                  int64_t* launches);
+                  int64_t* launches, int* gate = nullptr);
 
 }  // namespace hb

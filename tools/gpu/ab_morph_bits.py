@@ -68,14 +68,14 @@ for opn in ("erode", "dilate"):
     res, outs = [], []
     for nob in (False, True):
         if nob:
-            os.environ["HB_MORPH_NOBITS"] = "1"
+            os.environ["HB_MORPH_NOBITS"] = "1"; os.environ["HB_MORPH_BITS1"] = "1"
         else:
-            os.environ.pop("HB_MORPH_NOBITS", None)
+            os.environ.pop("HB_MORPH_NOBITS", None); os.environ.pop("HB_MORPH_BITS1", None)
         ms = timeit(x, o, prog, 3)
         outs.append(o.clone())
         v = n * n * nzo / ms / 1e6
         res.append(f"{'bytes' if nob else 'bits'} {v:7.1f} Gvox/s ({ms:.3f} ms, {2 * v / 6445.6:.3f} of HBM)")
-    os.environ.pop("HB_MORPH_NOBITS", None)
+    os.environ.pop("HB_MORPH_NOBITS", None); os.environ.pop("HB_MORPH_BITS1", None)
     same = bool(torch.equal(outs[0], outs[1]))
     bad += not same
     print(f"{opn} ball:3 u8 binary 2048^2 x {nzo}: " + " | ".join(res) + f" | identical {same}", flush=True)
