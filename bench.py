@@ -516,8 +516,9 @@ def _timeit(fn, stream, reps=5):
 
 
 def side_filters(n, peak, stream):
-    """configs[0] (gaussian sigma=2 on 256^3, single chunk) and the configs[1]
-    mean r=1 on n^3, device-resident — reported beside the headline."""
+    """configs[0] (gaussian sigma=2 on 256^3, single chunk), the configs[1]
+    mean r=1 on n^3 and configs[2]'s erosion (ball:3, u16 grey and u8 binary,
+    2048^2 planes), device-resident — reported beside the headline."""
     import torch
 
     from paper_2511_11890_b200 import _native, filters
@@ -551,6 +552,27 @@ def side_filters(n, peak, stream):
     res[f"mean_r1_{n}"] = {"gvox_s": round(n ** 3 / ms / 1e6, 3), "ms": round(ms, 4),
                            "hbm_frac": round(8 * n ** 3 / ms / 1e6 / peak, 4)}
     del x, o
+    torch.cuda.synchronize()
+    # configs[2]: erosion ball:3 on 2048^2-plane slabs, u16 grey and u8 binary
+    # (a 256-slice slab per launch: local ops are size-invariant per slice)
+    from paper_2511_11890_b200 import morphology
+
+    se = morphology.StructuringElement.parse("ball:3")
+    prog = morphology.morph_program("erode", se)
+    m, nzs = 2048, 256
+    for name, dt, make, bpv in (
+            ("erode_ball3_u16_2048", torch.uint16,
+             lambda: torch.randint(0, 65536, (nzs + 6, m, m), device="cuda", dtype=torch.int32).to(torch.uint16), 4),
+            ("erode_ball3_u8_binary_2048", torch.uint8,
+             lambda: (torch.rand((nzs + 6, m, m), device="cuda") < 0.5).to(torch.uint8), 2)):
+        x = make()
+        o = torch.empty((nzs, m, m), device="cuda", dtype=dt)
+        ms = _timeit(lambda: _native.apply_device(x, o, prog, 3, stream), stream)
+        v = m * m * nzs
+        res[name] = {"gvox_s": round(v / ms / 1e6, 3), "ms": round(ms, 4),
+                     "hbm_frac": round(bpv * v / ms / 1e6 / peak, 4),
+                     "kernel": "k_morph3<u16>" if dt == torch.uint16 else "k_morph_bits2"}
+        del x, o
     torch.cuda.synchronize()
     return res
 
