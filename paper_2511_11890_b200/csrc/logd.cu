@@ -25,6 +25,9 @@ namespace hb {
 namespace {
 
 constexpr int LX = 128;  // x columns per warp
+#ifndef HB_LOG_MINB
+#define HB_LOG_MINB 4  // 128 registers: 16 warps/SM instead of 8 at 179 (LoG 1024^3: 111.6 vs 95-106 Gvox/s; 5-6 spill)
+#endif
 
 struct LogArgs {
   const float* g;
@@ -61,7 +64,7 @@ __device__ __forceinline__ float comp(const float4& v, int c) {
 }
 
 template <int RY, int W>
-__global__ void __launch_bounds__(32 * W) k_log_stream(const LogArgs a) {
+__global__ void __launch_bounds__(32 * W, HB_LOG_MINB) k_log_stream(const LogArgs a) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int x0 = blockIdx.x * LX;
   const int xl = x0 + 4 * lane;
