@@ -147,6 +147,34 @@ class Clocks:
 # --------------------------------------------------------------------------
 # distributed plumbing
 # --------------------------------------------------------------------------
+_NUMA_CPUS = None
+_ALL_CPUS = None
+
+
+def bind_numa_local(dev):
+    """Pin this process to the CPUs local to GPU `dev` (NVML's ideal
+    affinity) before any pinned host buffer is touched: first-touch then puts
+    the staging memory on the GPU's NUMA node, so H2D/D2H DMA does not cross
+    the socket link (the e2e and out-of-core numbers are PCIe-bound).
+    Best effort: returns the CPU count bound to, or None."""
+    global _ALL_CPUS
+    try:
+        import pynvml
+
+        _ALL_CPUS = os.sched_getaffinity(0)
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(dev)
+        words = pynvml.nvmlDeviceGetCpuAffinity(h, 8)  # 8 x 64-bit words = 512 CPUs
+        cpus = {64 * i + b for i, w in enumerate(words) for b in range(64) if (w >> b) & 1}
+        cpus &= set(range(os.cpu_count() or 1))
+        if cpus:
+            os.sched_setaffinity(0, cpus)
+            return len(cpus)
+    except Exception:
+        return None
+    return None
+
+
 def dist_setup(args):
     import torch
 
@@ -169,6 +197,8 @@ def dist_setup(args):
             dist.init_process_group("gloo")
             _DIST_DEVICE = "cpu"
     os.environ["HARPIA_DEVICE"] = str(dev)
+    global _NUMA_CPUS
+    _NUMA_CPUS = bind_numa_local(dev)
     local = dev
     return world, rank, local
 
@@ -406,10 +436,15 @@ def run_ours(args):
 
     cpu = parity = None
     if rank == 0 and world == 1 and not args.no_cpu:
+        # the CPU baselines use every host core, not just the GPU's NUMA node
+        local_cpus = os.sched_getaffinity(0)
+        if _ALL_CPUS:
+            os.sched_setaffinity(0, _ALL_CPUS)
         cpu, parity = cpu_baseline_and_parity(x, out_g, out_m, n)
         rp = reference_python_sample(n)
         if rp is not None:
             cpu["reference_python"] = rp
+        os.sched_setaffinity(0, local_cpus)
     del x, out_g, out_m
     torch.cuda.synchronize()
     filters_out.update(side_filters(n, peak, stream))
@@ -460,6 +495,7 @@ def run_ours(args):
                "d2h_bytes_per_step": int(r1.d2h_bytes + r2.d2h_bytes),
                "chunks_per_op": [r1.chunk_count, r2.chunk_count], "steps": e2e_steps,
                "device_residual_bytes": int(r1.device_residual_bytes + r2.device_residual_bytes),
+               "numa_local_cpus": _NUMA_CPUS,
                "path": "registry.run_operator('gaussian', sigma=2) + ('median', r=1) -> hb_run "
                        "(pinned in/out, 4+ chunks, halos), inside one device-arena session"}
         gpu_launches += sum(a.kernel_launches + b.kernel_launches for a, b in reps)

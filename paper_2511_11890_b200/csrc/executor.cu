@@ -1609,7 +1609,12 @@ static int32_t run_host_range(const hb_volume* in, hb_volume* out,
   const size_t cap = free_b > (256u << 20) ? free_b - (256u << 20) : 0;
   size_t soft = cap;
   if (ex->device_budget > 0) soft = std::min(cap, (size_t)ex->device_budget);
-  const size_t target = (size_t)160 << 20;  // ~160 MiB per pipeline slot
+  // ~160 MiB per pipeline slot (HB_SLOT_MB overrides: smaller slots shorten
+  // the pipeline fill / drain of a job, larger ones cut per-piece overhead)
+  static const size_t target = [] {
+    const char* v = std::getenv("HB_SLOT_MB");
+    return (size_t)(v ? std::max(8, std::atoi(v)) : 160) << 20;
+  }();
   int64_t S = max_int;
   while (S > 1 && slot_bytes_for(S) > target && S > 2 * H) S = std::max<int64_t>(1, S * 3 / 4);
   int depth = ex->pipeline_depth > 0 ? ex->pipeline_depth : 3;
