@@ -528,6 +528,21 @@ struct SeShape {
 
 constexpr int M3X_TX = 64, M3X_TY = 32, M3X_NT = 512, M3X_NST = 3;
 constexpr int M3X_Q = M3X_TX / 4;  // 4-wide x blocks per row (16)
+// output rows per V/Z thread: 2 for grey data — each staged H row a thread
+// loads serves two output rows, cutting the shared-memory reads of the layer
+// folds that bounded the kernel (ncu: LSU 66%, LDS barrier/mio stalls) —
+// and 1 for the binary AND/OR variant
+#ifndef HB_M3X_MINB
+#define HB_M3X_MINB 3
+#endif
+#ifndef HB_M3X_VR
+#define HB_M3X_VR 2  // u16 ball:3 2048^2: VR 1 576, 2 598 (at 3 CTAs/SM), 4 spills (518)
+#endif
+template <bool BIN> struct M3XV {
+  static constexpr int VR = BIN ? 1 : HB_M3X_VR;
+  static constexpr int NT = M3X_Q * (M3X_TY / VR);
+  static constexpr int MINB = BIN ? 2 : HB_M3X_MINB;  // resident CTAs the register budget is sized for
+};
 
 struct Morph3Args {
   int nzi, zo, nzo, zchunk, nx, ny;
@@ -559,7 +574,7 @@ __device__ __forceinline__ uint32_t mop3(uint32_t a, uint32_t b, uint32_t c) {
 }
 
 template <typename T, bool MAX, int KIND, int R, bool BIN>
-__global__ void __launch_bounds__(M3X_NT, 2)
+__global__ void __launch_bounds__(M3XV<BIN>::NT, M3XV<BIN>::MINB)
 k_morph3(const __grid_constant__ CUtensorMap tin, T* __restrict__ out, const Morph3Args a,
          const int* __restrict__ gate) {
   static_assert(!BIN || sizeof(T) == 1, "the binary path is uint8 only");
@@ -601,14 +616,18 @@ k_morph3(const __grid_constant__ CUtensorMap tin, T* __restrict__ out, const Mor
   }
   __syncthreads();
 
-  // V/Z ownership: row vy, 4-wide x block vq (two u16x2 words: pairs 2vq, 2vq+1)
-  const int vq = tid % M3X_Q, vy = tid / M3X_Q;  // vy in [0, 32)
-  uint32_t acc[RING][NW];
+  // V/Z ownership: rows vy .. vy+VR-1, 4-wide x block vq (two u16x2 words:
+  // pairs 2vq, 2vq+1)
+  constexpr int VR = M3XV<BIN>::VR, NTK = M3XV<BIN>::NT;
+  const int vq = tid % M3X_Q, vy = (tid / M3X_Q) * VR;  // vy in [0, 32)
+  uint32_t acc[RING][VR][NW];
   constexpr uint32_t IDENT = MAX ? 0u : 0xffffffffu;
 #pragma unroll
   for (int u = 0; u < RING; ++u)
 #pragma unroll
-    for (int j = 0; j < NW; ++j) acc[u][j] = IDENT;
+    for (int t = 0; t < VR; ++t)
+#pragma unroll
+      for (int j = 0; j < NW; ++j) acc[u][t][j] = IDENT;
 
   // load the u16x2 word covering x = (tile) 2p, 2p+1 of stage row r
   auto word = [&](const T* row, int p) -> uint32_t {
@@ -622,12 +641,13 @@ k_morph3(const __grid_constant__ CUtensorMap tin, T* __restrict__ out, const Mor
 
   // output pointer of local output slice 0 and this thread's store shape
   const int gy = y0 + vy, gx = x0 + 4 * vq;
-  const bool st_full = gy < a.ny && gx + 3 < a.nx;
-  const bool st_part = gy < a.ny && gx < a.nx && !st_full;
+  const bool st_x = gx + 3 < a.nx, st_xp = gx < a.nx && !st_x;
   T* const obase = out + ((int64_t)z0 * a.ny + min(gy, a.ny - 1)) * (int64_t)a.nx + min(gx, a.nx - 1);
   const int64_t oplane = (int64_t)a.ny * a.nx;
-  auto store_out = [&](int o, uint32_t v0, uint32_t v1) {
-    T* dst = obase + o * oplane;
+  auto store_out = [&](int o, int t, uint32_t v0, uint32_t v1) {
+    const bool st_full = gy + t < a.ny && st_x;
+    const bool st_part = gy + t < a.ny && st_xp;
+    T* dst = obase + o * oplane + (gy + t < a.ny ? t : 0) * (int64_t)a.nx;
     if constexpr (BIN) {
       if (st_full) *reinterpret_cast<uint32_t*>(dst) = v0;
       else if (st_part)
@@ -648,7 +668,7 @@ k_morph3(const __grid_constant__ CUtensorMap tin, T* __restrict__ out, const Mor
     T* stage = sraw + st * (STAGE_PITCH / sizeof(T));
     mbar_wait(&bar[st], (uint32_t)((s / M3X_NST) & 1));
     if (border) {
-      clamp_tile<T, M3X_NT>(stage, WBOX, HY, M3X_TX + 2 * XA2, y0 - R, x0 - XA2, a.ny, a.nx, tid);
+      clamp_tile<T, NTK>(stage, WBOX, HY, M3X_TX + 2 * XA2, y0 - R, x0 - XA2, a.ny, a.nx, tid);
       fence_proxy_async();
       __syncthreads();
     }
@@ -656,8 +676,8 @@ k_morph3(const __grid_constant__ CUtensorMap tin, T* __restrict__ out, const Mor
     if constexpr (R > 0) {
       // a compile-time trip count lets the per-item index math hoist out of the slice loop
 #pragma unroll
-      for (int it = 0; it < (HY * M3X_Q + M3X_NT - 1) / M3X_NT; ++it) {
-        const int item = tid + it * M3X_NT;
+      for (int it = 0; it < (HY * M3X_Q + NTK - 1) / NTK; ++it) {
+        const int item = tid + it * NTK;
         if (item >= HY * M3X_Q) break;
         const int r = item / M3X_Q, q = item % M3X_Q;
         const T* row = stage + r * WBOX;
@@ -720,10 +740,11 @@ k_morph3(const __grid_constant__ CUtensorMap tin, T* __restrict__ out, const Mor
     // ---- V: every layer's 2D shape for this thread's 4 outputs ----------------
     // rows of one layer are folded three at a time (VIMNMX3.U16x2); the two
     // words of a row come from one LDS.64; identical loads across layers CSE
-    uint32_t layer[R + 1][NW];
-    {
-      const uint32_t* hb = sH + (vy + R) * WPR + NW * vq;  // H_k row r: hb[((k-1)*HY + r-vy-R)*WPR]
-      const T* rb = stage + (vy + R) * WBOX + XA2 + 4 * vq;
+    uint32_t layer[VR][R + 1][NW];
+#pragma unroll
+    for (int t = 0; t < VR; ++t) {
+      const uint32_t* hb = sH + (vy + t + R) * WPR + NW * vq;  // H_k row r: hb[((k-1)*HY + r-vy-R)*WPR]
+      const T* rb = stage + (vy + t + R) * WBOX + XA2 + 4 * vq;
       auto term = [&](int k, int dy, int j) -> uint32_t {
         if (k == 0) {
           if constexpr (BIN) {
@@ -762,7 +783,7 @@ k_morph3(const __grid_constant__ CUtensorMap tin, T* __restrict__ out, const Mor
             ++nt;
           }
           if (has_pend) v = mop2<MAX, BIN>(v, pend);
-          layer[L][j] = v;
+          layer[t][L][j] = v;
         }
       }
     }
@@ -775,14 +796,16 @@ k_morph3(const __grid_constant__ CUtensorMap tin, T* __restrict__ out, const Mor
       _Pragma("unroll") for (int d = -R; d <= R; ++d) {                                 \
         const int slot = ((U - d - R) % RING + RING) % RING; /* o = s - d - R */        \
         const int L = d < 0 ? -d : d;                                                   \
+        _Pragma("unroll") for (int t = 0; t < VR; ++t) {                                \
         if (d == R) {                                                                   \
-          const uint32_t v0 = mop2<MAX, BIN>(acc[slot][0], layer[L][0]);                \
-          const uint32_t v1 = NW > 1 ? mop2<MAX, BIN>(acc[slot][NW - 1], layer[L][NW - 1]) : 0u; \
-          if (s >= 2 * R) store_out(s - 2 * R, v0, v1);                                 \
-          _Pragma("unroll") for (int j = 0; j < NW; ++j) acc[slot][j] = IDENT;          \
+          const uint32_t v0 = mop2<MAX, BIN>(acc[slot][t][0], layer[t][L][0]);          \
+          const uint32_t v1 = NW > 1 ? mop2<MAX, BIN>(acc[slot][t][NW - 1], layer[t][L][NW - 1]) : 0u; \
+          if (s >= 2 * R) store_out(s - 2 * R, t, v0, v1);                              \
+          _Pragma("unroll") for (int j = 0; j < NW; ++j) acc[slot][t][j] = IDENT;       \
         } else {                                                                        \
           _Pragma("unroll") for (int j = 0; j < NW; ++j)                                \
-            acc[slot][j] = mop2<MAX, BIN>(acc[slot][j], layer[L][j]);                   \
+            acc[slot][t][j] = mop2<MAX, BIN>(acc[slot][t][j], layer[t][L][j]);          \
+        }                                                                               \
         }                                                                               \
       }                                                                                 \
     }                                                                                   \
@@ -857,7 +880,7 @@ cudaError_t launch_morph3_v(const DevIn& in, int64_t zo, int64_t nzo, void* out,
   dim3 grid(gx, gy, (unsigned)((nzo + a.zchunk - 1) / a.zchunk));
   auto kern = k_morph3<T, MAX, KIND, R, BIN>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  kern<<<grid, M3X_NT, smem, s>>>(tin, (T*)out, a, gate);
+  kern<<<grid, M3XV<BIN>::NT, smem, s>>>(tin, (T*)out, a, gate);
   return cudaGetLastError();
 }
 
