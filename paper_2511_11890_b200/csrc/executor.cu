@@ -437,6 +437,18 @@ cudaError_t run_stage_impl(const StageDesc& d, const DevIn& in, int64_t zo, int6
         epi.orig_zo = zo;
         epi.amount = d.amount;
       }
+      if (d.precision == HB_PREC_FAST && epi.kind == EPI_NONE && in.dt == HB_F32 &&
+          (in.nx < 384 || in.ny < 384)) {
+        // small planes: split passes (gauss_small.cu) instead of z-streaming
+        float* tmp = (float*)pa.get((size_t)nzo * plane * 4);
+        if (tmp) {
+          cudaError_t e = gaussian_small(in, zo, nzo, (float*)out, d.taps, epi, tmp, s, launches);
+          if (e != cudaErrorNotSupported) return e;
+        } else {
+          pa.err = cudaSuccess;
+        }
+        cudaGetLastError();
+      }
       if (d.precision == HB_PREC_FAST) {
         cudaError_t e = gaussian_fused(in, zo, nzo, (float*)out, d.taps, epi, s, launches);
         if (e != cudaErrorNotSupported) return e;

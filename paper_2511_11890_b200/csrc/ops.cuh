@@ -95,6 +95,8 @@ cudaError_t copy_slices(const DevIn& in, int64_t zo, int64_t nzo, void* out,
 // Returns cudaErrorNotSupported when the shape/radius is outside the fused
 // kernel's envelope; the caller then uses the generic path.
 // warp-specialised Gaussian / unsharp (gauss_ws.cu), 2 <= R <= 8, nx % 4 == 0
+cudaError_t gaussian_small(const DevIn& in, int64_t zo, int64_t nzo, float* out, const Taps& taps,
+                           const EpiArgs& epi, float* tmp, cudaStream_t s, int64_t* launches);
 cudaError_t gaussian_tri(const DevIn& in, int64_t zo, int64_t nzo, float* out, const Taps& taps,
                         const EpiArgs& epi, cudaStream_t s, int64_t* launches);
 cudaError_t gaussian_ws(const DevIn& in, int64_t zo, int64_t nzo, float* out, const Taps& taps,
