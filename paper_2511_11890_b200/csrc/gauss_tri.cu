@@ -121,8 +121,14 @@ __device__ __forceinline__ void clamp_stage(float* st, int pitch, int h, int w, 
   }
 }
 
+#ifndef HB_GTRI_NSY
+#define HB_GTRI_NSY 3
+#endif
+#ifndef HB_GTRI_NSX
+#define HB_GTRI_NSX 4  // sY/sX ring depths: 2/3, 3/4, 4/6 all within noise (305-309 Gvox/s)
+#endif
 #ifndef HB_GTRI_NST
-#define HB_GTRI_NST 10
+#define HB_GTRI_NST 14  // TMA stages: 10 -> 14 measured 308 -> 313 Gvox/s (216 KB of smem)
 #endif
 #ifndef HB_GTRI_TY
 #define HB_GTRI_TY 32  // 32: one 640-thread CTA/SM with setmaxnreg; 16: two 320-thread CTAs/SM (measured 265 vs 310 Gvox/s)
@@ -160,8 +166,8 @@ struct GeoT {
   static constexpr int WBOX = (XOFF + NYC + 3) / 4 * 4;
   static constexpr int STAGE_PITCH = (HB * WBOX * 4 + 127) / 128 * 128;
   static constexpr int NST = HB_GTRI_NST;   // TMA stages
-  static constexpr int NSY = 3;   // y-filtered slices
-  static constexpr int NSX = 4;   // xy-filtered slices
+  static constexpr int NSY = HB_GTRI_NSY;   // y-filtered slices
+  static constexpr int NSX = HB_GTRI_NSX;   // xy-filtered slices
   static constexpr int RING = 2 * R + 1;
   static constexpr int NYI = NYP * (TY / YR);
   static constexpr int SYP = (2 * NYC + 31) / 32 * 32;  // floats per row pair
