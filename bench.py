@@ -553,8 +553,9 @@ def _timeit(fn, stream, reps=5):
 
 def side_filters(n, peak, stream):
     """configs[0] (gaussian sigma=2 on 256^3, single chunk), the configs[1]
-    mean r=1 on n^3 and configs[2]'s erosion (ball:3, u16 grey and u8 binary,
-    2048^2 planes), device-resident — reported beside the headline."""
+    mean r=1 on n^3, configs[3]'s unsharp and exact LoG on n^3, the 5^3
+    median on a 256-slice slab and configs[2]'s erosion (ball:3, u16 grey and
+    u8 binary, 2048^2 planes), device-resident — reported beside the headline."""
     import torch
 
     from paper_2511_11890_b200 import _native, filters
@@ -587,6 +588,24 @@ def side_filters(n, peak, stream):
     ms = _timeit(lambda: _native.apply_device(x, o, prog, 1, stream), stream)
     res[f"mean_r1_{n}"] = {"gvox_s": round(n ** 3 / ms / 1e6, 3), "ms": round(ms, 4),
                            "hbm_frac": round(8 * n ** 3 / ms / 1e6 / peak, 4)}
+    del x, o
+    torch.cuda.synchronize()
+    # configs[3]'s two stages on n^3 (unsharp sigma=1 fast, LoG sigma=2 exact)
+    # and the north_star's 5^3 median (r=2, f32) on a 256-slice slab
+    x = torch.rand((n + 20, n, n), device="cuda")
+    o = torch.empty((n, n, n), device="cuda")
+    for name, prog, zb in ((f"unsharp_s1_{n}", filters.unsharp_program(1.0, 1.5), 10),
+                           (f"log_s2_exact_{n}", filters.log_program(2.0), 10)):
+        with _native.session():
+            ms = _timeit(lambda: _native.apply_device(x, o, prog, zb, stream), stream, reps=3)
+        res[name] = {"gvox_s": round(n ** 3 / ms / 1e6, 3), "ms": round(ms, 4),
+                     "hbm_frac": round(8 * n ** 3 / ms / 1e6 / peak, 4)}
+    del x, o
+    x = torch.rand((256 + 4, n, n), device="cuda")
+    o = torch.empty((256, n, n), device="cuda")
+    ms = _timeit(lambda: _native.apply_device(x, o, filters.median_program(2), 2, stream), stream, reps=2)
+    res[f"median_r2_{n}x{n}x256"] = {"gvox_s": round(256 * n * n / ms / 1e6, 3), "ms": round(ms, 4),
+                                     "hbm_frac": round(8 * 256 * n * n / ms / 1e6 / peak, 4)}
     del x, o
     torch.cuda.synchronize()
     # configs[2]: erosion ball:3 on 2048^2-plane slabs, u16 grey and u8 binary
