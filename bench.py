@@ -626,7 +626,7 @@ def side_filters(n, peak, stream):
         v = m * m * nzs
         res[name] = {"gvox_s": round(v / ms / 1e6, 3), "ms": round(ms, 4),
                      "hbm_frac": round(bpv * v / ms / 1e6 / peak, 4),
-                     "kernel": "k_morph3<u16>" if dt == torch.uint16 else "k_morph_bits2"}
+                     "kernel": "k_morph_u16s" if dt == torch.uint16 else "k_morph_bits2"}
         del x, o
     torch.cuda.synchronize()
     return res

@@ -1254,6 +1254,221 @@ cudaError_t launch_morph_bits(const DevIn& in, int64_t zo, int64_t nzo, void* ou
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// k_morph_u16s: grey u16 erosion / dilation (configs[2]'s u16 volumes) with
+// k_morph_bits2's register-streaming structure on u16x2 words instead of bits
+// (k_morph3 above stages every x-run in shared memory and re-reads it per
+// layer: LSU/barrier-bound at ~0.37 of HBM).  CTA tile = 128 columns x 32
+// rows, 8 warps; a thread owns 2 words (4 voxels) x 4 output rows and marches
+// z.  Per input slice (TMA box 144 x 38 u16, x0-8 .. x0+135, into a 4-deep
+// mbarrier ring):
+//   * each of its 4 + 2R rows is read as 3 LDS.64 (words w-2 .. w+3), the
+//     odd-start pairs come from 5 PRMTs shared by both words, and the x-runs
+//     h_k = op(h_{k-1}, x-k, x+k) are one VIMNMX3.U16x2 each;
+//   * rows are taken two at a time and every (dz, dy) row of the SE is folded
+//     into the accumulator of its output slice, two SE rows per VIMNMX3;
+//   * accumulators live in a (2R+1)-slot register ring indexed by the slice
+//     number mod 2R+1 (the slice loop is unrolled 2R+1 times, so completing
+//     an output is a store + reset, never a register shift).
+// Border tiles clamp the staged box (clamp_tile) before reading it.
+// ---------------------------------------------------------------------------
+constexpr int MU_TX = 128, MU_RO = 4, MU_WARPS = 8, MU_TY = MU_RO * MU_WARPS, MU_NST = 4;
+constexpr int MU_XA = 8;                     // box starts 8 voxels (16 B) left of the tile
+constexpr int MU_WBOX = MU_TX + 2 * MU_XA;   // 144 u16 = 288 B per staged row
+#ifndef HB_MU_MINB
+#define HB_MU_MINB 2
+#endif
+
+template <int R>
+struct MUGeo {
+  static constexpr int HY = MU_TY + 2 * R;
+  static constexpr int BOX = MU_WBOX * HY * 2;            // bytes
+  static constexpr int PITCH = (BOX + 127) / 128 * 128;
+  static constexpr int SMEM = MU_NST * PITCH + MU_NST * 8 + 128;
+};
+
+template <int V>
+struct IC {
+  static constexpr int value = V;
+};
+
+template <bool MAX, int KIND, int R>
+__global__ void __launch_bounds__(MU_WARPS * 32, HB_MU_MINB)
+k_morph_u16s(const __grid_constant__ CUtensorMap tin, uint16_t* __restrict__ out, const Morph3Args a) {
+  using S = SeShape<KIND, R>;
+  using G = MUGeo<R>;
+  constexpr int RING = 2 * R + 1, NROW = MU_RO + 2 * R;
+  constexpr uint32_t ID = MAX ? 0u : 0xffffffffu;
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + MU_NST * G::PITCH);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int x0 = blockIdx.x * MU_TX, y0 = blockIdx.y * MU_TY;
+  const int z0 = blockIdx.z * a.zchunk, z1 = min(z0 + a.zchunk, a.nzo);
+  const int nsl = (z1 - z0) + 2 * R;
+  auto zin = [&](int k) { return min(max(a.zo + z0 - R + k, 0), a.nzi - 1); };
+  if (tid == 0) {
+#pragma unroll
+    for (int i = 0; i < MU_NST; ++i) mbar_init(&bar[i], 1);
+    fence_mbar_init();
+    prefetch_tmap(&tin);
+    for (int i = 0; i < MU_NST && i < nsl; ++i) {
+      mbar_expect_tx(&bar[i], G::BOX);
+      tma_load_3d(smem + i * G::PITCH, &tin, x0 - MU_XA, y0 - R, zin(i), &bar[i]);
+    }
+  }
+  __syncthreads();
+  const bool border = x0 - MU_XA < 0 || x0 + MU_TX + MU_XA > a.nx || y0 - R < 0 || y0 + MU_TY + R > a.ny;
+  // this thread: voxels x0 + 4*lane .. +3 (words W[2], W[3]) of rows y0 + 4*warp .. +3
+  const int gx = x0 + 4 * lane, gy = y0 + MU_RO * warp;
+  // staged row r (0 .. NROW-1) of this thread = box row MU_RO*warp + r; words
+  // w-2 .. w+3 start at box column 4*lane + MU_XA - 4 (8-B aligned)
+  const int roff = (MU_RO * warp) * MU_WBOX * 2 + (4 * lane + MU_XA - 4) * 2;
+  const int64_t plane = (int64_t)a.ny * a.nx;
+  const bool st_full = gx + 3 < a.nx;
+  const bool st_part = gx < a.nx && !st_full;
+  uint16_t* obase = out + (int64_t)z0 * plane + (int64_t)min(gy, a.ny - 1) * a.nx + min(gx, a.nx - 1);
+  uint32_t A[RING][MU_RO][2];
+#pragma unroll
+  for (int u = 0; u < RING; ++u)
+#pragma unroll
+    for (int t = 0; t < MU_RO; ++t) A[u][t][0] = A[u][t][1] = ID;
+
+  int st = 0;
+  uint32_t ph = 0;
+  // x-runs h[k][j] (k = 0..R) of staged row r for words j = 0, 1
+  auto runs = [&](const unsigned char* stage, int r, uint32_t (&h)[R + 1][2]) {
+    const uint2* p = reinterpret_cast<const uint2*>(stage + roff + r * MU_WBOX * 2);
+    const uint2 q0 = p[0], q1 = p[1], q2 = p[2];
+    const uint32_t W[6] = {q0.x, q0.y, q1.x, q1.y, q2.x, q2.y};  // pairs 2w-2 .. 2w+3
+    uint32_t P[5];  // P[i] = (hi of W[i], lo of W[i+1]): odd-start pairs
+    // (IMAD.HI + IMAD on the idle FMA pipe instead of the PRMT measured 784
+    // vs 831 Gvox/s: the IMAD.HI rate)
+#pragma unroll
+    for (int i = 0; i < 5; ++i) P[i] = prmt(W[i], W[i + 1], 0x5432);
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      h[0][j] = W[2 + j];
+      if constexpr (R >= 1) h[1][j] = op3x2<MAX>(W[2 + j], P[1 + j], P[2 + j]);
+      if constexpr (R >= 2) h[2][j] = op3x2<MAX>(h[1][j], W[1 + j], W[3 + j]);
+      if constexpr (R >= 3) h[3][j] = op3x2<MAX>(h[2][j], P[j], P[3 + j]);
+    }
+  };
+  auto step = [&](auto Uc, int s) {
+    constexpr int U = decltype(Uc)::value;  // s % RING
+    unsigned char* stage = smem + st * G::PITCH;
+    mbar_wait(&bar[st], ph);
+    if (border) {
+      clamp_tile<uint16_t, MU_WARPS * 32>(reinterpret_cast<uint16_t*>(stage), MU_WBOX, G::HY, MU_WBOX,
+                                          y0 - R, x0 - MU_XA, a.ny, a.nx, tid);
+      __syncthreads();
+    }
+#pragma unroll
+    for (int r = 0; r < NROW; r += 2) {
+      uint32_t hA[R + 1][2], hB[R + 1][2];
+      runs(stage, r, hA);
+      const bool two = r + 1 < NROW;
+      if (two) runs(stage, r + 1, hB);
+#pragma unroll
+      for (int t = 0; t < MU_RO; ++t) {
+        const int dyA = r - R - t, dyB = dyA + 1;
+#pragma unroll
+        for (int j = 0; j < RING; ++j) {
+          // input slice s feeds output o = s - 2R + j at dz = R - j; its ring
+          // slot is o mod RING = (U + 1 + j) mod RING
+          const int slot = (U + 1 + j) % RING;
+          const int kA = (dyA >= -R && dyA <= R) ? S::hw(R - j, dyA) : -1;
+          const int kB = (two && dyB >= -R && dyB <= R) ? S::hw(R - j, dyB) : -1;
+#pragma unroll
+          for (int w = 0; w < 2; ++w) {
+            if (kA >= 0 && kB >= 0) A[slot][t][w] = op3x2<MAX>(A[slot][t][w], hA[kA][w], hB[kB][w]);
+            else if (kA >= 0) A[slot][t][w] = op2x2<MAX>(A[slot][t][w], hA[kA][w]);
+            else if (kB >= 0) A[slot][t][w] = op2x2<MAX>(A[slot][t][w], hB[kB][w]);
+          }
+        }
+      }
+    }
+    __syncthreads();  // every thread has read stage st
+    if (tid == 0 && s + MU_NST < nsl) {
+      fence_proxy_async();
+      mbar_expect_tx(&bar[st], G::BOX);
+      tma_load_3d(stage, &tin, x0 - MU_XA, y0 - R, zin(s + MU_NST), &bar[st]);
+    }
+    if (++st == MU_NST) { st = 0; ph ^= 1u; }
+    // output o = s - 2R is complete (slot (U + 1) mod RING)
+    constexpr int cs = (U + 1) % RING;
+    if (s >= 2 * R) {
+      uint16_t* op = obase + (int64_t)(s - 2 * R) * plane;
+#pragma unroll
+      for (int t = 0; t < MU_RO; ++t) {
+        if (gy + t < a.ny) {
+          uint16_t* d = op + (int64_t)t * a.nx;
+          if (st_full) {
+            *reinterpret_cast<uint2*>(d) = make_uint2(A[cs][t][0], A[cs][t][1]);
+          } else if (st_part) {
+            for (int i = 0; i < 4 && gx + i < a.nx; ++i)
+              d[i] = (uint16_t)((A[cs][t][i >> 1] >> (16 * (i & 1))) & 0xffffu);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < MU_RO; ++t) A[cs][t][0] = A[cs][t][1] = ID;
+  };
+  for (int s = 0; s < nsl; s += RING) {
+    step(IC<0>{}, s);
+    if constexpr (RING > 1) { if (s + 1 >= nsl) break; step(IC<1 % RING>{}, s + 1); }
+    if constexpr (RING > 2) { if (s + 2 >= nsl) break; step(IC<2 % RING>{}, s + 2); }
+    if constexpr (RING > 3) { if (s + 3 >= nsl) break; step(IC<3 % RING>{}, s + 3); }
+    if constexpr (RING > 4) { if (s + 4 >= nsl) break; step(IC<4 % RING>{}, s + 4); }
+    if constexpr (RING > 5) { if (s + 5 >= nsl) break; step(IC<5 % RING>{}, s + 5); }
+    if constexpr (RING > 6) { if (s + 6 >= nsl) break; step(IC<6 % RING>{}, s + 6); }
+  }
+}
+
+// NotSupported outside the envelope (k_morph3 takes those): TMA layout (16-B
+// aligned base, nx % 8 == 0), extents < 2^30.  HB_MORPH_U16_SMEM=1 keeps
+// k_morph3 for u16 (A/B).
+template <bool MAX, int KIND, int R>
+cudaError_t launch_morph_u16s(const DevIn& in, int64_t zo, int64_t nzo, void* out, cudaStream_t s) {
+  using G = MUGeo<R>;
+  if (in.dt != HB_U16 || (in.nx % 8) != 0 || (reinterpret_cast<uintptr_t>(in.p) & 15) != 0 ||
+      in.nz >= (1 << 30) || in.ny >= (1 << 30) || in.nx >= (1 << 30) || std::getenv("HB_MORPH_U16_SMEM"))
+    return cudaErrorNotSupported;
+  CUtensorMap tin;
+  if (!make_tmap_3d(&tin, in.p, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, in.nx, in.ny, in.nz, MU_WBOX, G::HY))
+    return cudaErrorNotSupported;
+  auto kern = k_morph_u16s<MAX, KIND, R>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM) != cudaSuccess)
+    return cudaErrorNotSupported;
+  Morph3Args a;
+  a.nzi = (int)in.nz;
+  a.zo = (int)zo;
+  a.nzo = (int)nzo;
+  a.nx = (int)in.nx;
+  a.ny = (int)in.ny;
+  dim3 grid((unsigned)((in.nx + MU_TX - 1) / MU_TX), (unsigned)((in.ny + MU_TY - 1) / MU_TY), 1);
+  const int64_t tiles = (int64_t)grid.x * grid.y, slots = (int64_t)HB_MU_MINB * kNumSMs;
+  // z-chunks: wave-quantised cost, capped (HB_MU_ZCAP, default 128; 2048^2
+  // x 256 ball:3: 16 691, 32 781, 64 832, 128 836, 256 839 Gvox/s)
+  const char* zv = std::getenv("HB_MU_ZCAP");
+  const int64_t zcap = zv ? std::max(8, std::atoi(zv)) : 128;
+  int zchunk = (int)std::min<int64_t>(nzo, 16);
+  double best = 1e300;
+  for (int64_t zc = 16; zc <= std::max<int64_t>(16, std::min<int64_t>(nzo, zcap)); zc += 8) {
+    const int64_t ctas = tiles * ((nzo + zc - 1) / zc);
+    const double cost = (double)((ctas + slots - 1) / slots) * (double)(zc + 2 * R);
+    if (cost < best * 0.995) {
+      best = cost;
+      zchunk = (int)zc;
+    }
+  }
+  a.zchunk = (int)std::min<int64_t>(zchunk, std::max<int64_t>(1, nzo));
+  grid.z = (unsigned)((nzo + a.zchunk - 1) / a.zchunk);
+  kern<<<grid, MU_WARPS * 32, G::SMEM, s>>>(tin, (uint16_t*)out, a);
+  return cudaGetLastError();
+}
+
 __global__ void k_u8_grey_check(const uint8_t* __restrict__ p, int64_t n, int* __restrict__ grey) {
   const int64_t n16 = n / 16;
   bool any = false;
@@ -1273,6 +1488,9 @@ template <typename T, bool MAX, int KIND, int R>
 cudaError_t launch_morph3(const DevIn& in, int64_t zo, int64_t nzo, void* out, cudaStream_t s,
                           int* gate_scratch) {
   if constexpr (sizeof(T) == 2) {
+    const cudaError_t e = launch_morph_u16s<MAX, KIND, R>(in, zo, nzo, out, s);
+    if (e != cudaErrorNotSupported) return e;
+    cudaGetLastError();
     return launch_morph3_v<T, MAX, KIND, R, false>(in, zo, nzo, out, nullptr, s);
   } else {
     if ((reinterpret_cast<uintptr_t>(in.p) & 15) != 0 || std::getenv("HB_MORPH_NOBIN"))

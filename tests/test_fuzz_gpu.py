@@ -2,8 +2,9 @@
 infrastructure): random extents around every tile / chunk boundary the
 kernels have — k_gauss_tri (planes >= 384^2, 48x32 tiles, capped z-chunks),
 the small-plane split passes (gauss_small.cu), k_median3_f32 (64x8 tiles,
-TMA box at x0-4), k_morph_bits2 (64-row x 256-voxel tiles, halo words) and
-the two-rows-per-thread grey k_morph3 — through the public API (chunked,
+TMA box at x0-4), k_morph_bits2 (64-row x 256-voxel tiles, halo words), the
+register-streaming grey u16 k_morph_u16s (128 x 32 tiles, nx % 8 == 0) and
+the two-rows-per-thread grey k_morph3 (other widths) — through the public API (chunked,
 halos), bit-exact where the operator is exact, <= 1e-5 otherwise."""
 import numpy as np
 import pytest
@@ -60,5 +61,9 @@ def test_fuzz_morphology(oracle, case):
     b = (rng.random((nz, ny, nx)) < 0.55).astype(np.uint8)
     assert np.array_equal(morphology.erode(b, se), oracle.erode(b, se.offsets)), (spec, b.shape)
     assert np.array_equal(morphology.dilate(b, se), oracle.dilate(b, se.reflect().offsets)), (spec, b.shape)
-    g = rng.integers(0, 65536, size=(nz, ny, nx + 4)).astype(np.uint16)
+    g = rng.integers(0, 65536, size=(nz, ny, nx + 4)).astype(np.uint16)  # k_morph3
     assert np.array_equal(morphology.erode(g, se), oracle.erode(g, se.offsets)), (spec, g.shape)
+    nx8 = 8 * int(rng.integers(1, 70))  # k_morph_u16s: ragged 128-column tiles
+    g = rng.integers(0, 65536, size=(nz, ny, nx8)).astype(np.uint16)
+    assert np.array_equal(morphology.erode(g, se), oracle.erode(g, se.offsets)), (spec, g.shape)
+    assert np.array_equal(morphology.dilate(g, se), oracle.dilate(g, se.reflect().offsets)), (spec, g.shape)

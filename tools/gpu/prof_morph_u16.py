@@ -1,4 +1,4 @@
-"""One launch of the grey u16 ball:3 erosion (k_morph3) on a 2048^2 x 256 slab, for ncu."""
+"""One launch of the grey u16 ball:3 erosion (k_morph_u16s; HB_MORPH_U16_SMEM=1: k_morph3) on a 2048^2 x 256 slab, for ncu."""
 import sys
 import torch
 sys.path.insert(0, ".")

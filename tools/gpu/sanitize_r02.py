@@ -1,6 +1,6 @@
 """compute-sanitizer sweep of the round-2 kernels on small shapes:
 k_gauss_tri (planes >= 384^2, ragged tiles, z-chunks, unsharp), k_median3_f32
-(ragged x/y, border tiles), k_morph_bits (binary + flagged grey blocks)."""
+(ragged x/y, border tiles), k_morph_bits (binary + flagged grey blocks), k_morph_u16s (grey u16)."""
 import sys
 import numpy as np
 sys.path.insert(0, '.')
@@ -19,4 +19,8 @@ for shape, spec in [((12, 37, 64), "ball:3"), ((9, 20, 96), "box:2"), ((7, 40, 3
     morphology.dilate(b, se)
     g = rng.integers(0, 256, size=shape).astype(np.uint8)
     morphology.erode(g, se)
+    # k_morph_u16s: grey u16 (border tiles, ragged rows / columns, z-chunks)
+    w = rng.integers(0, 65536, size=(shape[0], shape[1] + 3, shape[2] + 8)).astype(np.uint16)
+    morphology.erode(w, se)
+    morphology.dilate(w, se)
 print("sanitize sweep done")
