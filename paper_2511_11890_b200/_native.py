@@ -19,7 +19,9 @@ import numpy as np
 
 from .errors import HB_OK, ParameterError, UnsupportedFormatError, raise_for_status
 
-LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libharpia_b200.so"
+# HARPIA_LIB: developer A/B of library builds (tools/gpu/ab_*.py); default in-tree
+LIB_PATH = Path(os.environ.get("HARPIA_LIB") or
+                Path(__file__).resolve().parent / "_lib" / "libharpia_b200.so")
 
 # enum values of include/harpia_b200.h
 HB_U8, HB_U16, HB_U32, HB_F32 = 0, 1, 2, 3

@@ -31,6 +31,12 @@
 namespace hb {
 namespace {
 
+#ifndef HB_M3_ASM_EMIT
+#define HB_M3_ASM_EMIT 0
+#endif
+#ifndef HB_M3_SHARED_ROWSUM
+#define HB_M3_SHARED_ROWSUM 1  // x-row sorts of the two outputs share r1 + r2 (one IMAD fewer per row)
+#endif
 #ifndef HB_M3_ALU_EVERY
 #define HB_M3_ALU_EVERY 0  // merge exchanges in ALU form: 1, 2, 3 measured 226, 238, 240 vs 244 Gvox/s at 0
 #endif
@@ -103,10 +109,21 @@ struct NetF {
     int a[3][3], b[3][3];
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
+#if HB_M3_SHARED_ROWSUM
+      // the two rows share r1, r2: their sum once, each middle = total - min - max
+      const int s12 = imad(r[i][1], one, r[i][2]);
+      a[i][0] = fmn3(r[i][0], r[i][1], r[i][2]);
+      a[i][2] = fmx3(r[i][0], r[i][1], r[i][2]);
+      a[i][1] = imad(a[i][2], mone, imad(a[i][0], mone, imad(r[i][0], one, s12)));
+      b[i][0] = fmn3(r[i][1], r[i][2], r[i][3]);
+      b[i][2] = fmx3(r[i][1], r[i][2], r[i][3]);
+      b[i][1] = imad(b[i][2], mone, imad(b[i][0], mone, imad(r[i][3], one, s12)));
+#else
       a[i][0] = r[i][0]; a[i][1] = r[i][1]; a[i][2] = r[i][2];
       b[i][0] = r[i][1]; b[i][1] = r[i][2]; b[i][2] = r[i][3];
       sort3(a[i][0], a[i][1], a[i][2]);
       sort3(b[i][0], b[i][1], b[i][2]);
+#endif
     }
     tableau(a, pa);
     tableau(b, pb);
@@ -254,6 +271,7 @@ k_median3_f32(const __grid_constant__ CUtensorMap tin, float* __restrict__ out,
   // predicated stores (no divergent branch around them)
   const bool single0 = !pair_store && st_y && st_x0, single1 = !pair_store && st_y && st_x1;
   auto emit = [&](int m0, int m1) {
+#if HB_M3_ASM_EMIT
     asm volatile(
         "{\n.reg .pred p, q, r;\n"
         "setp.ne.b32 p, %3, 0;\n setp.ne.b32 q, %4, 0;\n setp.ne.b32 r, %5, 0;\n"
@@ -262,6 +280,15 @@ k_median3_f32(const __grid_constant__ CUtensorMap tin, float* __restrict__ out,
         "@r st.global.b32 [%0+4], %2;\n}\n" ::"l"(optr),
         "r"(m0), "r"(m1), "r"((int)pair_store), "r"((int)single0), "r"((int)single1)
         : "memory");
+#else
+    // loop-invariant predicates (the asm form re-derived them per store)
+    if (pair_store) {
+      *reinterpret_cast<int2*>(optr) = make_int2(m0, m1);
+    } else {
+      if (single0) reinterpret_cast<int*>(optr)[0] = m0;
+      if (single1) reinterpret_cast<int*>(optr)[1] = m1;
+    }
+#endif
     optr += plane;
   };
   int X[2][9], Y[2][9], Z[2][9], W[2][9], M[2][10];
