@@ -31,6 +31,9 @@
 namespace hb {
 namespace {
 
+#ifndef HB_M3_TAB_IMAD
+#define HB_M3_TAB_IMAD 0
+#endif
 #ifndef HB_M3_ASM_EMIT
 #define HB_M3_ASM_EMIT 0
 #endif
@@ -99,8 +102,12 @@ struct NetF {
   __device__ __forceinline__ void tableau(const int (&m)[3][3], int (&s)[9]) const {
     s[0] = m[0][0]; s[1] = m[0][1]; s[2] = m[1][0]; s[3] = m[0][2]; s[4] = m[1][1];
     s[5] = m[2][0]; s[6] = m[1][2]; s[7] = m[2][1]; s[8] = m[2][2];
-    ce_alu(s[3], s[5]); ce_alu(s[1], s[2]); ce_alu(s[2], s[3]); ce_alu(s[6], s[7]);
-    ce_alu(s[5], s[6]); ce_alu(s[3], s[4]); ce_alu(s[4], s[5]);
+    // the first HB_M3_TAB_IMAD exchanges in min + IMAD form, the rest ALU-only
+    // (balances the ALU pipe against issue)
+#define HB_TCE(n, i, j) if ((n) < HB_M3_TAB_IMAD) ce(s[i], s[j]); else ce_alu(s[i], s[j]);
+    HB_TCE(0, 3, 5) HB_TCE(1, 1, 2) HB_TCE(2, 2, 3) HB_TCE(3, 6, 7)
+    HB_TCE(4, 5, 6) HB_TCE(5, 3, 4) HB_TCE(6, 4, 5)
+#undef HB_TCE
   }
   // sorted planes of the two x-adjacent outputs from r[row][x-1 .. x+2]
   __device__ __forceinline__ void planes2(int (&r)[3][4], int (&pa)[9], int (&pb)[9]) const {
