@@ -518,6 +518,18 @@ struct SeShape {
     const int rem = R * R - dz * dz - dy * dy;
     return rem < 0 ? -1 : isqrt(rem);
   }
+  // number of rows (dy) of layer |dz| = L, and its dy extent
+  static constexpr __host__ __device__ int nterms(int L) {
+    int n = 0;
+    for (int dy = -R; dy <= R; ++dy) n += hw(L, dy) >= 0;
+    return n;
+  }
+  static constexpr __host__ __device__ int dyext(int L) {
+    int e = -1;
+    for (int dy = 0; dy <= R; ++dy)
+      if (hw(L, dy) >= 0) e = dy;
+    return e;
+  }
   static constexpr __host__ __device__ bool needs(int k) {  // is run half-width k used anywhere?
     for (int dz = 0; dz <= R; ++dz)
       for (int dy = 0; dy <= R; ++dy)
@@ -1265,13 +1277,20 @@ cudaError_t launch_morph_bits(const DevIn& in, int64_t zo, int64_t nzo, void* ou
 //   * each of its 4 + 2R rows is read as 3 LDS.64 (words w-2 .. w+3), the
 //     odd-start pairs come from 5 PRMTs shared by both words, and the x-runs
 //     h_k = op(h_{k-1}, x-k, x+k) are one VIMNMX3.U16x2 each;
-//   * rows are taken two at a time and every (dz, dy) row of the SE is folded
-//     into the accumulator of its output slice, two SE rows per VIMNMX3;
+//   * rows are taken two at a time; the dz = 0 rows of the SE are folded
+//     straight into their accumulator (two SE rows per VIMNMX3, the
+//     accumulator is the third operand), the rows of each layer |dz| = L > 0
+//     are reduced to the 2D layer once and that is folded into both the +L
+//     and the -L accumulator (ball:3: 14 instead of 18 VIMNMX per output
+//     word; HB_MU_DIRECT=1 builds the all-direct form);
 //   * accumulators live in a (2R+1)-slot register ring indexed by the slice
 //     number mod 2R+1 (the slice loop is unrolled 2R+1 times, so completing
 //     an output is a store + reset, never a register shift).
 // Border tiles clamp the staged box (clamp_tile) before reading it.
 // ---------------------------------------------------------------------------
+#ifndef HB_MU_DIRECT
+#define HB_MU_DIRECT 0  // 1: every SE row folded straight into its accumulators (no shared +/-dz layers)
+#endif
 constexpr int MU_TX = 128, MU_RO = 4, MU_WARPS = 8, MU_TY = MU_RO * MU_WARPS, MU_NST = 4;
 constexpr int MU_XA = 8;                     // box starts 8 voxels (16 B) left of the tile
 constexpr int MU_WBOX = MU_TX + 2 * MU_XA;   // 144 u16 = 288 B per staged row
@@ -1363,6 +1382,7 @@ k_morph_u16s(const __grid_constant__ CUtensorMap tin, uint16_t* __restrict__ out
                                           y0 - R, x0 - MU_XA, a.ny, a.nx, tid);
       __syncthreads();
     }
+    uint32_t LP[MU_RO][R + 1][2];  // 2D layers |dz| = L in construction
 #pragma unroll
     for (int r = 0; r < NROW; r += 2) {
       uint32_t hA[R + 1][2], hB[R + 1][2];
@@ -1373,17 +1393,45 @@ k_morph_u16s(const __grid_constant__ CUtensorMap tin, uint16_t* __restrict__ out
       for (int t = 0; t < MU_RO; ++t) {
         const int dyA = r - R - t, dyB = dyA + 1;
 #pragma unroll
-        for (int j = 0; j < RING; ++j) {
+        for (int L = 0; L <= R; ++L) {
+          const int kA = (dyA >= -R && dyA <= R) ? S::hw(L, dyA) : -1;
+          const int kB = (two && dyB >= -R && dyB <= R) ? S::hw(L, dyB) : -1;
+          if (kA < 0 && kB < 0) continue;
           // input slice s feeds output o = s - 2R + j at dz = R - j; its ring
-          // slot is o mod RING = (U + 1 + j) mod RING
-          const int slot = (U + 1 + j) % RING;
-          const int kA = (dyA >= -R && dyA <= R) ? S::hw(R - j, dyA) : -1;
-          const int kB = (two && dyB >= -R && dyB <= R) ? S::hw(R - j, dyB) : -1;
+          // slot is o mod RING = (U + 1 + j) mod RING.  Layer |dz| = L.
+          const int sp = (U + 1 + R - L) % RING, sm = (U + 1 + R + L) % RING;
+          if (HB_MU_DIRECT || L == 0 || S::nterms(L) == 1) {
+            // straight into the accumulator(s): the accumulator is the third
+            // operand of every VIMNMX3
 #pragma unroll
-          for (int w = 0; w < 2; ++w) {
-            if (kA >= 0 && kB >= 0) A[slot][t][w] = op3x2<MAX>(A[slot][t][w], hA[kA][w], hB[kB][w]);
-            else if (kA >= 0) A[slot][t][w] = op2x2<MAX>(A[slot][t][w], hA[kA][w]);
-            else if (kB >= 0) A[slot][t][w] = op2x2<MAX>(A[slot][t][w], hB[kB][w]);
+            for (int g = 0; g < (L == 0 ? 1 : 2); ++g) {
+              const int slot = g == 0 ? sp : sm;
+#pragma unroll
+              for (int w = 0; w < 2; ++w) {
+                if (kA >= 0 && kB >= 0) A[slot][t][w] = op3x2<MAX>(A[slot][t][w], hA[kA][w], hB[kB][w]);
+                else if (kA >= 0) A[slot][t][w] = op2x2<MAX>(A[slot][t][w], hA[kA][w]);
+                else A[slot][t][w] = op2x2<MAX>(A[slot][t][w], hB[kB][w]);
+              }
+            }
+          } else {
+            // dz = +L and -L take the same 2D layer: build it once (rows
+            // t+R+dymin .. t+R+dymax), then fold it into both accumulators
+            const int rf = t + R - S::dyext(L), rl = t + R + S::dyext(L);
+#pragma unroll
+            for (int w = 0; w < 2; ++w) {
+              uint32_t& lp = LP[t][L][w];
+              if (rf >= r) {  // the layer starts in this row pair
+                if (kA >= 0 && kB >= 0) lp = op2x2<MAX>(hA[kA][w], hB[kB][w]);
+                else lp = kA >= 0 ? hA[kA][w] : hB[kB][w];
+              } else {
+                if (kA >= 0 && kB >= 0) lp = op3x2<MAX>(lp, hA[kA][w], hB[kB][w]);
+                else lp = op2x2<MAX>(lp, kA >= 0 ? hA[kA][w] : hB[kB][w]);
+              }
+              if (rl <= r + 1) {  // complete
+                A[sp][t][w] = op2x2<MAX>(A[sp][t][w], lp);
+                A[sm][t][w] = op2x2<MAX>(A[sm][t][w], lp);
+              }
+            }
           }
         }
       }
