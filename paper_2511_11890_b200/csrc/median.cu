@@ -12,6 +12,7 @@
 
 #include "ops.cuh"
 #include "median_nets.h"
+#include "median5_nets.h"
 
 namespace hb {
 namespace {
@@ -224,6 +225,167 @@ k_median5_pair(const T* __restrict__ in, int64_t nz, int64_t ny, int64_t nx, int
       }
     }
   }
+}
+
+// ---- 5x5x5 by comparator networks, marching z (k_median5_net) --------------
+// Same band argument as k_median5_pair (C = the 4 planes shared by outputs z
+// and z+1, only C's ranks 37..62 can be either median), but with sorted planes
+// and data-oblivious networks (tools/netgen/median125.py) instead of
+// forgetful selection, and every plane sorted once per column as the thread
+// marches z (two outputs per step):
+//   S(p)  = the 25 samples of plane p sorted (SORT25, 152 CE);
+//   M     = merge(S(z-1), S(z)) carried from the previous step, M' =
+//           merge(S(z+1), S(z+2)) (MERGE25, 119 CE);
+//   band  = ranks 37..62 of M u M' (BAND, 85 CE + 74 single min/max);
+//   out z = rank 26 of band u S(z-2), out z+1 = rank 26 of band u S(z+3):
+//           min_j max(band[25-j], S[j-1]) (25 max + 13 three-input min).
+// ~2 x 152 + 119 + 85 CE per output pair instead of ~3700 forgetful
+// exchanges.  Sorted planes wait in shared memory ([slot][rank][thread]:
+// conflict-free, every index static); M stays in registers.  8/16-bit data
+// runs the networks on two x-adjacent outputs per register (U2).
+constexpr int M5_NT = 128;
+
+template <typename K>
+__device__ __forceinline__ K m5_select(const K (&band)[26], const K* u) {
+  K t[26];
+  t[0] = band[25];
+#pragma unroll
+  for (int j = 1; j <= 25; ++j) t[j] = MinMax<K>::mx(band[25 - j], u[(j - 1) * M5_NT]);
+#pragma unroll
+  for (int w = 26; w > 1; w = (w + 1) / 2) {
+#pragma unroll
+    for (int i = 0; i < w / 2; ++i) t[i] = MinMax<K>::mn(t[i], t[w - 1 - i]);
+  }
+  return t[0];
+}
+
+template <typename T, typename K, bool PACKED>
+__global__ void __launch_bounds__(M5_NT, 2)
+k_median5_net(const T* __restrict__ in, int64_t nz, int64_t ny, int64_t nx, int64_t zo, int64_t nzo,
+              int zchunk, T* __restrict__ out) {
+  extern __shared__ unsigned char m5_smem[];
+  K* sm = reinterpret_cast<K*>(m5_smem);  // [4 slots][25 ranks][M5_NT]
+  const int tid = threadIdx.x;
+  const int64_t px = PACKED ? (nx + 1) / 2 : nx;
+  const int64_t col = (int64_t)blockIdx.x * M5_NT + tid;
+  if (col >= ny * px) return;  // no CTA-wide synchronisation below
+  const int y = (int)(col / px);
+  const int x = (int)(col - (int64_t)y * px) * (PACKED ? 2 : 1);
+  const int64_t plane = ny * nx;
+  const int z0 = blockIdx.y * zchunk, z1 = (int)min((int64_t)z0 + zchunk, nzo);
+  Get5<K> g;
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    g.yo[k] = clampi(y + k - 2, 0, (int)ny - 1) * (int)nx;
+    g.xa[k] = clampi(x + k - 2, 0, (int)nx - 1);
+    g.xb[k] = clampi(x + 1 + k - 2, 0, (int)nx - 1);
+  }
+  // sorted plane of (output-relative) slice zr, in rank order in a[]
+  auto sortplane = [&](int zr, K (&a)[25]) {
+    g.sl[0] = in + clamp64(zo + zr, 0, nz - 1) * plane;
+    K w[25];
+#pragma unroll
+    for (int e = 0; e < 25; ++e) w[e] = load5<T, K>(g, 0, e);
+#define HB_CE(i, j) cs(w[i], w[j]);
+#define HB_MN(i, j) w[i] = MinMax<K>::mn(w[i], w[j]);
+#define HB_MX(i, j) w[j] = MinMax<K>::mx(w[i], w[j]);
+    HB_SORT25(HB_CE, HB_MN, HB_MX)
+    constexpr int o[25] = HB_SORT25_OUT;
+#pragma unroll
+    for (int k = 0; k < 25; ++k) a[k] = w[o[k]];
+  };
+  auto put = [&](int slot, const K (&a)[25]) {
+#pragma unroll
+    for (int k = 0; k < 25; ++k) sm[(slot * 25 + k) * M5_NT + tid] = a[k];
+  };
+  auto get = [&](int slot, K (&a)[25]) {
+#pragma unroll
+    for (int k = 0; k < 25; ++k) a[k] = sm[(slot * 25 + k) * M5_NT + tid];
+  };
+  auto merge = [&](const K (&a)[25], const K (&b)[25], K (&m)[50]) {
+    K w[50];
+#pragma unroll
+    for (int k = 0; k < 25; ++k) w[k] = a[k], w[25 + k] = b[k];
+    HB_MERGE25(HB_CE, HB_MN, HB_MX)
+    constexpr int o[50] = HB_MERGE25_OUT;
+#pragma unroll
+    for (int k = 0; k < 50; ++k) m[k] = w[o[k]];
+  };
+  K A[25], B[25], M[50];
+  int lo = 0, kk = 1, nn = 2, fr = 3;  // plane slots: S(z-2), S(z), S(z+1), free
+  sortplane(z0 - 2, A);
+  put(lo, A);
+  sortplane(z0 - 1, A);
+  sortplane(z0, B);
+  put(kk, B);
+  merge(A, B, M);
+  sortplane(z0 + 1, A);
+  put(nn, A);
+  for (int z = z0; z < z1; z += 2) {
+    K band[26];
+    {
+      sortplane(z + 2, A);
+      put(fr, A);
+      get(nn, B);
+      K Mn[50];
+      merge(B, A, Mn);  // M(z+1, z+2)
+      K w[100];
+#pragma unroll
+      for (int k = 0; k < 50; ++k) w[k] = M[k], w[50 + k] = Mn[k];
+      HB_BAND(HB_CE, HB_MN, HB_MX)
+      constexpr int o[26] = HB_BAND_OUT;
+#pragma unroll
+      for (int k = 0; k < 26; ++k) band[k] = w[o[k]];
+#pragma unroll
+      for (int k = 0; k < 50; ++k) M[k] = Mn[k];
+    }
+#undef HB_CE
+#undef HB_MN
+#undef HB_MX
+    const K r0 = m5_select<K>(band, sm + lo * 25 * M5_NT + tid);
+    sortplane(z + 3, A);
+    put(nn, A);  // S(z+3): the next step's S(z'+1)
+    const K r1 = m5_select<K>(band, sm + nn * 25 * M5_NT + tid);
+    const K res[2] = {r0, r1};
+#pragma unroll
+    for (int o = 0; o < 2; ++o) {
+      if (z + o >= z1) break;
+      T* op = out + (int64_t)(z + o) * plane + (int64_t)y * nx + x;
+      if constexpr (PACKED) {
+        const unsigned v = reinterpret_cast<const U2&>(res[o]).v;
+        op[0] = (T)(v & 0xffffu);
+        if (x + 1 < nx) op[1] = (T)(v >> 16);
+      } else {
+        op[0] = (T)res[o];
+      }
+    }
+    const int t = lo;
+    lo = kk;
+    kk = fr;
+    fr = t;
+  }
+}
+
+template <typename T, typename K, bool PACKED>
+cudaError_t launch_median5_net(const T* src, const DevIn& in, int64_t zo, int64_t nzo, T* dst,
+                               cudaStream_t s) {
+  const int64_t px = PACKED ? (in.nx + 1) / 2 : in.nx;
+  const int64_t cols = in.ny * px;
+  if (cols <= 0 || nzo <= 0 || in.nz >= (1LL << 30) || in.ny * in.nx >= (1LL << 31)) return cudaErrorNotSupported;
+  const int64_t nblk = (cols + M5_NT - 1) / M5_NT;
+  if (nblk > 0x7fffffffLL) return cudaErrorNotSupported;
+  // z-chunks: >= ~4 waves of 2 CTAs/SM; each chunk pays a 4-plane prologue
+  const int64_t want = std::max<int64_t>(1, (8 * kNumSMs + nblk - 1) / nblk);
+  int64_t zc = std::max<int64_t>(16, (nzo + want - 1) / want);
+  zc = std::min<int64_t>(zc + (zc & 1), std::max<int64_t>(2, nzo + (nzo & 1)));
+  const int64_t nch = (nzo + zc - 1) / zc;
+  if (nch > 65535) return cudaErrorNotSupported;
+  const int smem = 4 * 25 * M5_NT * (int)sizeof(K);
+  auto kern = k_median5_net<T, K, PACKED>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+    return cudaErrorNotSupported;
+  kern<<<dim3((unsigned)nblk, (unsigned)nch), M5_NT, smem, s>>>(src, in.nz, in.ny, in.nx, zo, nzo, (int)zc, dst);
+  return cudaGetLastError();
 }
 
 template <int R, typename T>
@@ -822,6 +984,16 @@ cudaError_t run_median(const DevIn& in, int64_t zo, int64_t nzo, void* out, int 
     k_median3_plane<T><<<grid, 256, 0, s>>>(src, in.nz, in.ny, in.nx, zo, nzo, zchunk, dst,
                                             ImadOnes{1, -1});
   } else if (r == 2) {
+    if (!std::getenv("HB_MEDIAN5_FORGETFUL") && !std::getenv("HB_MEDIAN5_SINGLE")) {
+      cudaError_t e;
+      if constexpr (sizeof(T) <= 2) e = launch_median5_net<T, U2, true>(src, in, zo, nzo, dst, s);
+      else e = launch_median5_net<T, K, false>(src, in, zo, nzo, dst, s);
+      if (e != cudaErrorNotSupported) {
+        if (launches) *launches += 1;
+        return e;
+      }
+      cudaGetLastError();
+    }
     if (!std::getenv("HB_MEDIAN5_SINGLE")) {
       const int64_t pairs = ((nzo + 1) / 2) * in.ny * (sizeof(T) <= 2 ? (in.nx + 1) / 2 : in.nx);
       const int gp = grid_for(pairs);
