@@ -164,6 +164,27 @@ def test_c1_1024_median_mean_gaussian_sampled(torch_dev, oracle):
 
 
 # --------------------------------------------------------------------------
+# the 5x5x5 median (north star's "3x3x3/5x5x5 median") on the bench's
+# 1024^2 x 256 block: k_median5_net's z-chunks, slab-sampled, bit-exact
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("dt", ["f32", "u16"])
+def test_median5_1024_sampled(torch_dev, oracle, dt):
+    from paper_2511_11890_b200 import filters
+
+    torch = torch_dev
+    g = torch.Generator(device="cuda").manual_seed(55)
+    if dt == "f32":
+        x = torch.rand((260, 1024, 1024), generator=g, device="cuda")
+    else:
+        x = torch.randint(0, 65536, (260, 1024, 1024), generator=g, device="cuda",
+                          dtype=torch.int32).to(torch.uint16)
+    out = _apply(torch, x, filters.median_program(2), 2)
+    _slab_check(x, out, 2, (0, 1, 2, 127, 128, 254, 255), lambda s: oracle.median(s, 2), exact=True)
+    del out, x
+    torch.cuda.empty_cache()
+
+
+# --------------------------------------------------------------------------
 # configs[2]: erode / dilate ball:3 on 2048^3 u16 and binary u8 (> 2^31 voxels)
 # --------------------------------------------------------------------------
 @pytest.mark.parametrize("dt", ["u16", "bin"])

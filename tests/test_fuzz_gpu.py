@@ -4,7 +4,8 @@ kernels have — k_gauss_tri (planes >= 384^2, 48x32 tiles, capped z-chunks),
 the small-plane split passes (gauss_small.cu), k_median3_f32 (64x8 tiles,
 TMA box at x0-4), k_morph_bits2 (64-row x 256-voxel tiles, halo words), the
 register-streaming grey u16 k_morph_u16s (128 x 32 tiles, nx % 8 == 0) and
-the two-rows-per-thread grey k_morph3 (other widths) — through the public API (chunked,
+the two-rows-per-thread grey k_morph3 (other widths), and the 5x5x5
+k_median5_net — through the public API (chunked,
 halos), bit-exact where the operator is exact, <= 1e-5 otherwise."""
 import numpy as np
 import pytest
@@ -67,3 +68,22 @@ def test_fuzz_morphology(oracle, case):
     g = rng.integers(0, 65536, size=(nz, ny, nx8)).astype(np.uint16)
     assert np.array_equal(morphology.erode(g, se), oracle.erode(g, se.offsets)), (spec, g.shape)
     assert np.array_equal(morphology.dilate(g, se), oracle.dilate(g, se.reflect().offsets)), (spec, g.shape)
+
+
+@pytest.mark.parametrize("case", range(10))
+def test_fuzz_median5(oracle, case):
+    """k_median5_net: ragged columns (128-thread CTAs over y*x), z-chunks of any
+    parity, tiny planes; f32 with repeats and signed zeros, packed u16 / u8."""
+    from paper_2511_11890_b200 import filters
+
+    rng = np.random.default_rng(5000 + case)
+    shape = (int(rng.integers(1, 24)), int(rng.integers(1, 60)), int(rng.integers(1, 140)))
+    dt = [np.float32, np.uint16, np.uint8][case % 3]
+    if dt == np.float32:
+        x = (rng.random(shape, dtype=np.float32) - 0.5).astype(np.float32)
+        x[rng.random(shape) < 0.1] = 0.25
+        x[rng.random(shape) < 0.05] = -0.0
+        x[rng.random(shape) < 0.05] = 0.0
+    else:
+        x = rng.integers(0, np.iinfo(dt).max, size=shape).astype(dt)
+    assert np.array_equal(filters.median(x, 2), oracle.median(x, 2)), (shape, dt)

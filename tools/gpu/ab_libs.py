@@ -2,7 +2,8 @@
 of one operator on a synthetic volume, output checksum compared across builds.
 
 usage: python tools/gpu/ab_libs.py OP N lib1.so lib2.so ...
-  OP: median (r=1 f32), gaussian (sigma=2 fast f32), erode_u16 (ball:3)."""
+  OP: median (r=1 f32), gaussian (sigma=2 fast f32), erode_u16 (ball:3), median5 /
+  median5_u16 (r=2 on N x 1024^2)."""
 import json
 import os
 import subprocess
@@ -15,7 +16,14 @@ from paper_2511_11890_b200 import _native, filters, morphology
 op, n = sys.argv[1], int(sys.argv[2])
 s = torch.cuda.current_stream()
 g = torch.Generator(device="cuda").manual_seed(5)
-if op == "erode_u16":
+if op in ("median5", "median5_u16"):
+    if op == "median5":
+        x = torch.rand((n + 4, 1024, 1024), generator=g, device="cuda")
+    else:
+        x = torch.randint(0, 65536, (n + 4, 1024, 1024), generator=g, device="cuda", dtype=torch.int32).to(torch.uint16)
+    o = torch.empty((n, 1024, 1024), device="cuda", dtype=x.dtype)
+    prog, zb = filters.median_program(2), 2
+elif op == "erode_u16":
     x = torch.randint(0, 65536, (n + 6, 2048, 2048), generator=g, device="cuda", dtype=torch.int32).to(torch.uint16)
     o = torch.empty((n, 2048, 2048), device="cuda", dtype=torch.uint16)
     prog, zb = morphology.morph_program("erode", morphology.StructuringElement.ball(3)), 3
