@@ -605,7 +605,8 @@ def side_filters(n, peak, stream):
     o = torch.empty((256, n, n), device="cuda")
     ms = _timeit(lambda: _native.apply_device(x, o, filters.median_program(2), 2, stream), stream, reps=2)
     res[f"median_r2_{n}x{n}x256"] = {"gvox_s": round(256 * n * n / ms / 1e6, 3), "ms": round(ms, 4),
-                                     "hbm_frac": round(8 * 256 * n * n / ms / 1e6 / peak, 4)}
+                                     "hbm_frac": round(8 * 256 * n * n / ms / 1e6 / peak, 4),
+                                     "kernel": "k_median5_net"}
     del x, o
     torch.cuda.synchronize()
     # configs[2]: erosion ball:3 on 2048^2-plane slabs, u16 grey and u8 binary
