@@ -240,8 +240,9 @@ k_median5_pair(const T* __restrict__ in, int64_t nz, int64_t ny, int64_t nx, int
 //   out z = rank 26 of band u S(z-2), out z+1 = rank 26 of band u S(z+3):
 //           min_j max(band[25-j], S[j-1]) (25 max + 13 three-input min).
 // ~2 x 152 + 119 + 85 CE per output pair instead of ~3700 forgetful
-// exchanges.  Sorted planes wait in shared memory ([slot][rank][thread]:
-// conflict-free, every index static); M stays in registers.  8/16-bit data
+// exchanges.  Sorted planes and M wait in shared memory ([slot][rank][thread]:
+// conflict-free, every index static), which keeps the registers at the band
+// merge's 100 wires: 3 CTAs (12 warps) per SM.  8/16-bit data
 // runs the networks on two x-adjacent outputs per register (U2).
 constexpr int M5_NT = 128;
 #ifndef HB_M5_ALU_EVERY
@@ -285,11 +286,11 @@ __device__ __forceinline__ K m5_select(const K (&band)[26], const K* u) {
 }
 
 template <typename T, typename K, bool PACKED>
-__global__ void __launch_bounds__(M5_NT, 2)
+__global__ void __launch_bounds__(M5_NT, 3)
 k_median5_net(const T* __restrict__ in, int64_t nz, int64_t ny, int64_t nx, int64_t zo, int64_t nzo,
               int zchunk, T* __restrict__ out, int one, int mone) {
   extern __shared__ unsigned char m5_smem[];
-  K* sm = reinterpret_cast<K*>(m5_smem);  // [4 slots][25 ranks][M5_NT]
+  K* sm = reinterpret_cast<K*>(m5_smem);  // [3 plane slots][25 ranks] + [M: 50 ranks], x M5_NT
   const int tid = threadIdx.x;
   const int64_t px = PACKED ? (nx + 1) / 2 : nx;
   const int64_t col = (int64_t)blockIdx.x * M5_NT + tid;
@@ -325,6 +326,10 @@ k_median5_net(const T* __restrict__ in, int64_t nz, int64_t ny, int64_t nx, int6
 #pragma unroll
     for (int k = 0; k < 25; ++k) sm[(slot * 25 + k) * M5_NT + tid] = a[k];
   };
+  auto putm = [&](const K (&m)[50]) {
+#pragma unroll
+    for (int k = 0; k < 50; ++k) sm[(3 * 25 + k) * M5_NT + tid] = m[k];
+  };
   auto get = [&](int slot, K (&a)[25]) {
 #pragma unroll
     for (int k = 0; k < 25; ++k) a[k] = sm[(slot * 25 + k) * M5_NT + tid];
@@ -339,42 +344,51 @@ k_median5_net(const T* __restrict__ in, int64_t nz, int64_t ny, int64_t nx, int6
 #pragma unroll
     for (int k = 0; k < 50; ++k) m[k] = w[o[k]];
   };
-  K A[25], B[25], M[50];
-  int lo = 0, kk = 1, nn = 2, fr = 3;  // plane slots: S(z-2), S(z), S(z+1), free
-  sortplane(z0 - 2, A);
-  put(lo, A);
-  sortplane(z0 - 1, A);
-  sortplane(z0, B);
-  put(kk, B);
-  merge(A, B, M);
-  sortplane(z0 + 1, A);
-  put(nn, A);
+  K A[25], B[25];
+  int lo = 0, kk = 1, nn = 2;  // plane slots: S(z-2), S(z), S(z+1)
+  {
+    K M[50];
+    sortplane(z0 - 2, A);
+    put(lo, A);
+    sortplane(z0 - 1, A);
+    sortplane(z0, B);
+    put(kk, B);
+    merge(A, B, M);
+    putm(M);
+    sortplane(z0 + 1, A);
+    put(nn, A);
+  }
   for (int z = z0; z < z1; z += 2) {
     K band[26];
     {
       sortplane(z + 2, A);
-      put(fr, A);
-      get(nn, B);
-      K Mn[50];
-      merge(B, A, Mn);  // M(z+1, z+2)
+      get(nn, B);  // S(z+1)
+      put(nn, A);  // S(z+2) takes its slot (the next step's S(z'))
       K w[100];
+      {
+        K Mn[50];
+        merge(B, A, Mn);  // M(z+1, z+2)
 #pragma unroll
-      for (int k = 0; k < 50; ++k) w[k] = M[k], w[50 + k] = Mn[k];
+        for (int k = 0; k < 50; ++k) w[50 + k] = Mn[k];
+      }
+#pragma unroll
+      for (int k = 0; k < 50; ++k) {
+        w[k] = sm[(3 * 25 + k) * M5_NT + tid];  // M(z-1, z)
+        sm[(3 * 25 + k) * M5_NT + tid] = w[50 + k];
+      }
       int nce = 0;
       HB_BAND(HB_CE, HB_MN, HB_MX)
       constexpr int o[26] = HB_BAND_OUT;
 #pragma unroll
       for (int k = 0; k < 26; ++k) band[k] = w[o[k]];
-#pragma unroll
-      for (int k = 0; k < 50; ++k) M[k] = Mn[k];
     }
 #undef HB_CE
 #undef HB_MN
 #undef HB_MX
     const K r0 = m5_select<K>(band, sm + lo * 25 * M5_NT + tid);
     sortplane(z + 3, A);
-    put(nn, A);  // S(z+3): the next step's S(z'+1)
-    const K r1 = m5_select<K>(band, sm + nn * 25 * M5_NT + tid);
+    put(lo, A);  // S(z+3): the next step's S(z'+1)
+    const K r1 = m5_select<K>(band, sm + lo * 25 * M5_NT + tid);
     const K res[2] = {r0, r1};
 #pragma unroll
     for (int o = 0; o < 2; ++o) {
@@ -388,10 +402,11 @@ k_median5_net(const T* __restrict__ in, int64_t nz, int64_t ny, int64_t nx, int6
         op[0] = (T)res[o];
       }
     }
+    // S(z') = S(z+2) sits in nn, S(z'+1) = S(z+3) in lo, S(z'-2) = S(z) in kk
     const int t = lo;
     lo = kk;
-    kk = fr;
-    fr = t;
+    kk = nn;
+    nn = t;
   }
 }
 
@@ -403,13 +418,13 @@ cudaError_t launch_median5_net(const T* src, const DevIn& in, int64_t zo, int64_
   if (cols <= 0 || nzo <= 0 || in.nz >= (1LL << 30) || in.ny * in.nx >= (1LL << 31)) return cudaErrorNotSupported;
   const int64_t nblk = (cols + M5_NT - 1) / M5_NT;
   if (nblk > 0x7fffffffLL) return cudaErrorNotSupported;
-  // z-chunks: >= ~4 waves of 2 CTAs/SM; each chunk pays a 4-plane prologue
-  const int64_t want = std::max<int64_t>(1, (8 * kNumSMs + nblk - 1) / nblk);
+  // z-chunks: >= ~4 waves of 3 CTAs/SM; each chunk pays a 4-plane prologue
+  const int64_t want = std::max<int64_t>(1, (12 * kNumSMs + nblk - 1) / nblk);
   int64_t zc = std::max<int64_t>(16, (nzo + want - 1) / want);
   zc = std::min<int64_t>(zc + (zc & 1), std::max<int64_t>(2, nzo + (nzo & 1)));
   const int64_t nch = (nzo + zc - 1) / zc;
   if (nch > 65535) return cudaErrorNotSupported;
-  const int smem = 4 * 25 * M5_NT * (int)sizeof(K);
+  const int smem = (3 * 25 + 50) * M5_NT * (int)sizeof(K);
   auto kern = k_median5_net<T, K, PACKED>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
     return cudaErrorNotSupported;
