@@ -143,7 +143,13 @@ constexpr int NT = NYT + NXT + NZT;                                    // 640 at
 // setmaxnreg (warpgroup-wide; an .inc draws only on what this CTA's .dec
 // released): launch at 96, Y -> 56 and X -> 80 free 5120 + 2048 registers,
 // the Z warps take 384 x 16 of them
-constexpr int kLaunchRegs = 96, kYRegs = 56, kXRegs = 80, kZRegs = 112;
+#ifndef HB_GTRI_YREGS
+#define HB_GTRI_YREGS 56
+#endif
+#ifndef HB_GTRI_XREGS
+#define HB_GTRI_XREGS 80
+#endif
+constexpr int kLaunchRegs = 96, kYRegs = HB_GTRI_YREGS, kXRegs = HB_GTRI_XREGS, kZRegs = 112;
 static_assert(NYT * (kLaunchRegs - kYRegs) + NXT * (kLaunchRegs - kXRegs) >= NZT * (kZRegs - kLaunchRegs),
               "register hand-over does not balance");
 

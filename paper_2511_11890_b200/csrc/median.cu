@@ -245,6 +245,9 @@ k_median5_pair(const T* __restrict__ in, int64_t nz, int64_t ny, int64_t nx, int
 // merge's 100 wires: 3 CTAs (12 warps) per SM.  8/16-bit data
 // runs the networks on two x-adjacent outputs per register (U2).
 constexpr int M5_NT = 128;
+#ifndef HB_M5_MINB_PACKED
+#define HB_M5_MINB_PACKED 3  // u8/u16: 3 CTAs/SM spill ~80 B of the packed loads and still win (u16 49.6 vs 47.5 Gvox/s at 2)
+#endif
 #ifndef HB_M5_ALU_EVERY
 #define HB_M5_ALU_EVERY 2  // every n-th exchange in min+max (ALU) form, the rest min + IMAD pair (1024^2x256 f32: 0 23.7, 1 24.3, 2 27.1, 3 27.0 Gvox/s)
 #endif
@@ -286,7 +289,7 @@ __device__ __forceinline__ K m5_select(const K (&band)[26], const K* u) {
 }
 
 template <typename T, typename K, bool PACKED>
-__global__ void __launch_bounds__(M5_NT, 3)
+__global__ void __launch_bounds__(M5_NT, PACKED ? HB_M5_MINB_PACKED : 3)
 k_median5_net(const T* __restrict__ in, int64_t nz, int64_t ny, int64_t nx, int64_t zo, int64_t nzo,
               int zchunk, T* __restrict__ out, int one, int mone) {
   extern __shared__ unsigned char m5_smem[];
