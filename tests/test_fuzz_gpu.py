@@ -87,3 +87,31 @@ def test_fuzz_median5(oracle, case):
     else:
         x = rng.integers(0, np.iinfo(dt).max, size=shape).astype(dt)
     assert np.array_equal(filters.median(x, 2), oracle.median(x, 2)), (shape, dt)
+
+
+@pytest.mark.parametrize("shape", [(300, 6, 40), (97, 3, 17), (131, 33, 8)])
+def test_median5_many_z_chunks(oracle, shape):
+    """Small planes make k_median5_net split z into many 16-slice chunks (odd
+    and even lengths, a ragged last chunk): every chunk's 4-plane prologue and
+    the pair stepping across chunk ends must reproduce the oracle."""
+    from paper_2511_11890_b200 import filters
+
+    rng = np.random.default_rng(sum(shape))
+    x = (rng.random(shape, dtype=np.float32) - 0.5).astype(np.float32)
+    x[rng.random(shape) < 0.1] = 0.125
+    assert np.array_equal(filters.median(x, 2), oracle.median(x, 2)), shape
+    u = rng.integers(0, 65536, size=shape).astype(np.uint16)
+    assert np.array_equal(filters.median(u, 2), oracle.median(u, 2)), shape
+
+
+@pytest.mark.parametrize("spec", ["ball:3", "box:1", "cross:2"])
+def test_morph_u16s_many_z_chunks(oracle, spec):
+    """k_morph_u16s on a small plane: z split into several chunks (the
+    accumulator ring restarts per chunk) with a ragged tail."""
+    from paper_2511_11890_b200 import morphology
+
+    rng = np.random.default_rng(77)
+    g = rng.integers(0, 65536, size=(101, 40, 64)).astype(np.uint16)
+    se = morphology.StructuringElement.parse(spec)
+    assert np.array_equal(morphology.erode(g, se), oracle.erode(g, se.offsets)), spec
+    assert np.array_equal(morphology.dilate(g, se), oracle.dilate(g, se.reflect().offsets)), spec
