@@ -129,6 +129,9 @@ k_fast_z2(const __grid_constant__ CUtensorMap tin, float* __restrict__ tmp, cons
       }
     }
   }
+  // let the Y/X pass's CTAs be scheduled once every Z CTA got here (they
+  // still wait for this grid's completion before reading tmp)
+  asm volatile("griddepcontrol.launch_dependents;");
 }
 
 // ---- Y + X pass of one slice tile ------------------------------------------------
@@ -166,6 +169,11 @@ k_fast_yx(const __grid_constant__ CUtensorMap tm, float* __restrict__ out, const
   if (tid == 0) {
     mbar_init(bar, 1);
     fence_mbar_init();
+    prefetch_tmap(&tm);
+    // programmatic dependent launch: everything above overlaps the Z pass's
+    // tail; tmp is read only after the Z grid has completed (no-op when the
+    // kernel is launched without the PDL attribute)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     mbar_expect_tx(bar, G::HB * G::WBOX * 4);
     tma_load_3d(sIn, &tm, x0 - G::XA, y0 - R, z, bar);
   }
@@ -274,7 +282,11 @@ cudaError_t launch_small(const DevIn& in, int64_t zo, int64_t nzo, float* out, c
     }
   }
   a.zchunk = (int)best_zc;
-  k_fast_z2<R><<<dim3(gx, gy, (unsigned)((nzo + best_zc - 1) / best_zc)), SZ_NT, 0, s>>>(tz, tmp, a);
+  const dim3 gz(gx, gy, (unsigned)((nzo + best_zc - 1) / best_zc));
+  // (one TMA pipeline per warp — 64-float row boxes, no CTA barrier per
+  // slice — measured 80-82 vs 78 us at 256^3: the small boxes cost more than
+  // the barrier)
+  k_fast_z2<R><<<gz, SZ_NT, 0, s>>>(tz, tmp, a);
   auto k = k_fast_yx<R>;
   if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM) != cudaSuccess)
     return cudaErrorNotSupported;
@@ -284,7 +296,22 @@ cudaError_t launch_small(const DevIn& in, int64_t zo, int64_t nzo, float* out, c
     // (the tensor map addresses tmp's slices from 0; offset the batch by
     // shifting the output pointer and using a map over the batch's slices)
     if (zb == 0) {
-      k<<<grid, SY_NT, G::SMEM, s>>>(tm, out, a);
+      if (!std::getenv("HB_SMALL_NO_PDL")) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = grid;
+        cfg.blockDim = dim3(SY_NT);
+        cfg.dynamicSmemBytes = G::SMEM;
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        const cudaError_t e = cudaLaunchKernelEx(&cfg, k, tm, out, a);
+        if (e != cudaSuccess) return e;
+      } else {
+        k<<<grid, SY_NT, G::SMEM, s>>>(tm, out, a);
+      }
     } else {
       CUtensorMap tb;
       if (!make_tmap_3d(&tb, tmp + zb * in.ny * in.nx, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, in.nx, in.ny,
