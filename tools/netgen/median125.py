@@ -1,7 +1,7 @@
 """Comparator networks for the 5x5x5 median (k_median5_net, median.cu):
 
-  SORT25  : 25 samples of one (y, x) plane -> ascending (sort5 columns, then
-            pruned odd-even merges);
+  SORT25  : 25 samples of one (y, x) plane -> ascending (odd-even merge sort
+            on 32 wires with 7 +inf pads, pruned: 138 CE);
   MERGE25 : two sorted 25-lists (wires 0..24, 25..49) -> sorted 50;
   BAND    : two sorted 50-lists (wires 0..49, 50..99) -> ranks 37..62 of the
             100 (the only ranks of the 4 shared planes that can be the median
@@ -72,18 +72,39 @@ class Builder:
 SORT5 = [(0, 1), (3, 4), (2, 4), (2, 3), (0, 3), (0, 2), (1, 4), (1, 3), (1, 2)]
 
 
+def oddeven_sort_net(n):
+    """Batcher odd-even merge sort of n = 2^k positions."""
+    net = []
+
+    def sort(lo, n):
+        if n > 1:
+            m = n // 2
+            sort(lo, m)
+            sort(lo + m, m)
+            net.extend(oddeven_merge_net(n, lo))
+
+    sort(0, n)
+    return net
+
+
+# +inf pad positions of the 32-wire odd-even merge sort (random search over
+# placements: 138 comparators after pruning; pads at the end give 140, the
+# sort5-columns + merge-tree construction 146-152)
+SORT25_PADS = (1, 3, 8, 13, 17, 19, 26)
+
+
 def sort25():
     b = Builder()
-    cols = []
-    for c in range(5):
-        w = [5 * c + i for i in range(5)]
-        for i, j in SORT5:
-            b.ops.append((w[i], w[j]))
-        cols.append(w)
-    m01 = b.merge(cols[0], cols[1])
-    m23 = b.merge(cols[2], cols[3])
-    m0123 = b.merge(m01, m23)
-    out = b.merge(m0123, cols[4])
+    pos, w = [], 0
+    for p in range(32):
+        if p in SORT25_PADS:
+            pos.append(INF)
+        else:
+            pos.append(w)
+            w += 1
+    b.apply(pos, oddeven_sort_net(32))
+    out = [x for x in pos if x is not INF]
+    assert len(out) == 25
     return b.ops, out
 
 
