@@ -310,11 +310,30 @@ k_median5_net(const T* __restrict__ in, int64_t nz, int64_t ny, int64_t nx, int6
     g.xb[k] = clampi(x + 1 + k - 2, 0, (int)nx - 1);
   }
   // sorted plane of (output-relative) slice zr, in rank order in a[]
+  // columns x-2 .. x+2 (+1 packed) all inside the volume: the 25 loads of a
+  // plane are 5 row pointers + immediate offsets (the clamped per-element
+  // address path costs ~3 integer ops per load)
+  const bool xin = x >= 2 && x + 2 + (PACKED ? 1 : 0) < nx;
   auto sortplane = [&](int zr, K (&a)[25]) {
     g.sl[0] = in + clamp64(zo + zr, 0, nz - 1) * plane;
     K w[25];
+    if (xin) {
 #pragma unroll
-    for (int e = 0; e < 25; ++e) w[e] = load5<T, K>(g, 0, e);
+      for (int dy = 0; dy < 5; ++dy) {
+        const T* r = (const T*)g.sl[0] + g.yo[dy] + (x - 2);
+#pragma unroll
+        for (int dx = 0; dx < 5; ++dx) {
+          if constexpr (PACKED) {
+            w[dy * 5 + dx] = m5_from<K>((int)((unsigned)__ldg(r + dx) | ((unsigned)__ldg(r + dx + 1) << 16)));
+          } else {
+            w[dy * 5 + dx] = (K)__ldg(r + dx);
+          }
+        }
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 25; ++e) w[e] = load5<T, K>(g, 0, e);
+    }
   int nce = 0;  // compile-time after unrolling
 #define HB_CE(i, j) \
   if (HB_M5_ALU_EVERY > 0 && (nce++ % HB_M5_ALU_EVERY) == 0) cs(w[i], w[j]); else m5_ce(w[i], w[j], one, mone);
