@@ -110,8 +110,17 @@ class Clocks:
             else:
                 self.h = nv.nvmlDeviceGetHandleByIndex(self.index)
             self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+            # warm the NVML query path (a cold first query on a fresh box took
+            # most of a short timed region: one sample), start polling, and
+            # only enter the timed region once the poller is running
+            nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+            nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
             self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
+            t0 = time.time()
+            while not self.samples and time.time() - t0 < 0.5:
+                time.sleep(0.001)
+            self.samples.clear()
         except Exception:
             self.nv = None
         return self
