@@ -274,16 +274,27 @@ __device__ __forceinline__ void m5_ce(K& a, K& b, int one, int mone) {
   a = lo;
 }
 
-template <typename K>
-__device__ __forceinline__ K m5_select(const K (&band)[26], const K* u) {
-  K t[26];
+template <typename K> __device__ __forceinline__ K m5_min3(K a, K b, K c) {
+  return MinMax<K>::mn(MinMax<K>::mn(a, b), c);  // ptxas: VIMNMX3 for the integer keys
+}
+template <> __device__ __forceinline__ float m5_min3<float>(float a, float b, float c) {
+  float r;
+  asm("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+// rank 26 of band (26, sorted) u the 25 sorted samples u(0..24):
+// min over j of max(band[25-j], u[j-1]) — 25 max, 13 three-input min
+template <typename K, typename U>
+__device__ __forceinline__ K m5_select(const K (&band)[26], U u) {
+  K t[27];
   t[0] = band[25];
 #pragma unroll
-  for (int j = 1; j <= 25; ++j) t[j] = MinMax<K>::mx(band[25 - j], u[(j - 1) * M5_NT]);
+  for (int j = 1; j <= 25; ++j) t[j] = MinMax<K>::mx(band[25 - j], u(j - 1));
+  t[26] = t[25];
 #pragma unroll
-  for (int w = 26; w > 1; w = (w + 1) / 2) {
+  for (int w = 27; w > 1; w /= 3) {
 #pragma unroll
-    for (int i = 0; i < w / 2; ++i) t[i] = MinMax<K>::mn(t[i], t[w - 1 - i]);
+    for (int i = 0; i < w / 3; ++i) t[i] = m5_min3<K>(t[3 * i], t[3 * i + 1], t[3 * i + 2]);
   }
   return t[0];
 }
@@ -407,10 +418,11 @@ k_median5_net(const T* __restrict__ in, int64_t nz, int64_t ny, int64_t nx, int6
 #undef HB_CE
 #undef HB_MN
 #undef HB_MX
-    const K r0 = m5_select<K>(band, sm + lo * 25 * M5_NT + tid);
+    const K* ulo = sm + lo * 25 * M5_NT + tid;
+    const K r0 = m5_select<K>(band, [&](int j) { return ulo[j * M5_NT]; });
     sortplane(z + 3, A);
     put(lo, A);  // S(z+3): the next step's S(z'+1)
-    const K r1 = m5_select<K>(band, sm + lo * 25 * M5_NT + tid);
+    const K r1 = m5_select<K>(band, [&](int j) { return A[j]; });  // S(z+3) still in registers
     const K res[2] = {r0, r1};
 #pragma unroll
     for (int o = 0; o < 2; ++o) {
