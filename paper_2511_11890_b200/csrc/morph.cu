@@ -1286,22 +1286,30 @@ cudaError_t launch_morph_bits(const DevIn& in, int64_t zo, int64_t nzo, void* ou
 //   * accumulators live in a (2R+1)-slot register ring indexed by the slice
 //     number mod 2R+1 (the slice loop is unrolled 2R+1 times, so completing
 //     an output is a store + reset, never a register shift).
-// Border tiles clamp the staged box (clamp_tile) before reading it.
+// Border tiles clamp the staged box (clamp_tile) before reading it.  Grey
+// u8 volumes run the same kernel on a 160-byte box, each staged byte pair
+// widened into u16 lanes by one PRMT (queued behind k_morph_bits2, which
+// flags the grey blocks; HB_MORPH_U8_SMEM=1 keeps k_morph3 for them).
 // ---------------------------------------------------------------------------
 #ifndef HB_MU_DIRECT
 #define HB_MU_DIRECT 0  // 1: every SE row folded straight into its accumulators (no shared +/-dz layers)
 #endif
 constexpr int MU_TX = 128, MU_RO = 4, MU_WARPS = 8, MU_TY = MU_RO * MU_WARPS, MU_NST = 4;
-constexpr int MU_XA = 8;                     // box starts 8 voxels (16 B) left of the tile
-constexpr int MU_WBOX = MU_TX + 2 * MU_XA;   // 144 u16 = 288 B per staged row
+// the box starts 16 B left of the tile: 8 u16 / 16 u8 voxels; staged rows
+// are 144 u16 (288 B) / 160 u8 (160 B)
+template <typename T> struct MUT {
+  static constexpr int XA = 16 / (int)sizeof(T);
+  static constexpr int WBOX = MU_TX + 2 * XA;
+  static constexpr int PB = WBOX * (int)sizeof(T);  // bytes per staged row
+};
 #ifndef HB_MU_MINB
 #define HB_MU_MINB 2
 #endif
 
-template <int R>
+template <typename T, int R>
 struct MUGeo {
   static constexpr int HY = MU_TY + 2 * R;
-  static constexpr int BOX = MU_WBOX * HY * 2;            // bytes
+  static constexpr int BOX = MUT<T>::PB * HY;            // bytes
   static constexpr int PITCH = (BOX + 127) / 128 * 128;
   static constexpr int SMEM = MU_NST * PITCH + MU_NST * 8 + 128;
 };
@@ -1311,11 +1319,16 @@ struct IC {
   static constexpr int value = V;
 };
 
-template <bool MAX, int KIND, int R>
+template <typename T, bool MAX, int KIND, int R>
 __global__ void __launch_bounds__(MU_WARPS * 32, HB_MU_MINB)
-k_morph_u16s(const __grid_constant__ CUtensorMap tin, uint16_t* __restrict__ out, const Morph3Args a) {
+k_morph_u16s(const __grid_constant__ CUtensorMap tin, T* __restrict__ out, const Morph3Args a,
+             const int* __restrict__ gate) {
+  // u8: queued behind k_morph_bits2, which flags grey blocks; a binary block
+  // is already done
+  if (gate != nullptr && *gate == 0) return;
   using S = SeShape<KIND, R>;
-  using G = MUGeo<R>;
+  using G = MUGeo<T, R>;
+  constexpr int MU_XA = MUT<T>::XA, MU_WBOX = MUT<T>::WBOX, PB = MUT<T>::PB;
   constexpr int RING = 2 * R + 1, NROW = MU_RO + 2 * R;
   constexpr uint32_t ID = MAX ? 0u : 0xffffffffu;
   extern __shared__ unsigned char smem_raw[];
@@ -1342,11 +1355,11 @@ k_morph_u16s(const __grid_constant__ CUtensorMap tin, uint16_t* __restrict__ out
   const int gx = x0 + 4 * lane, gy = y0 + MU_RO * warp;
   // staged row r (0 .. NROW-1) of this thread = box row MU_RO*warp + r; words
   // w-2 .. w+3 start at box column 4*lane + MU_XA - 4 (8-B aligned)
-  const int roff = (MU_RO * warp) * MU_WBOX * 2 + (4 * lane + MU_XA - 4) * 2;
+  const int roff = (MU_RO * warp) * PB + (4 * lane + MU_XA - 4) * (int)sizeof(T);
   const int64_t plane = (int64_t)a.ny * a.nx;
   const bool st_full = gx + 3 < a.nx;
   const bool st_part = gx < a.nx && !st_full;
-  uint16_t* obase = out + (int64_t)z0 * plane + (int64_t)min(gy, a.ny - 1) * a.nx + min(gx, a.nx - 1);
+  T* obase = out + (int64_t)z0 * plane + (int64_t)min(gy, a.ny - 1) * a.nx + min(gx, a.nx - 1);
   uint32_t A[RING][MU_RO][2];
 #pragma unroll
   for (int u = 0; u < RING; ++u)
@@ -1357,9 +1370,22 @@ k_morph_u16s(const __grid_constant__ CUtensorMap tin, uint16_t* __restrict__ out
   uint32_t ph = 0;
   // x-runs h[k][j] (k = 0..R) of staged row r for words j = 0, 1
   auto runs = [&](const unsigned char* stage, int r, uint32_t (&h)[R + 1][2]) {
-    const uint2* p = reinterpret_cast<const uint2*>(stage + roff + r * MU_WBOX * 2);
-    const uint2 q0 = p[0], q1 = p[1], q2 = p[2];
-    const uint32_t W[6] = {q0.x, q0.y, q1.x, q1.y, q2.x, q2.y};  // pairs 2w-2 .. 2w+3
+    uint32_t W[6];  // u16x2 pairs 2w-2 .. 2w+3
+    if constexpr (sizeof(T) == 2) {
+      const uint2* p = reinterpret_cast<const uint2*>(stage + roff + r * PB);
+      const uint2 q0 = p[0], q1 = p[1], q2 = p[2];
+      W[0] = q0.x, W[1] = q0.y, W[2] = q1.x, W[3] = q1.y, W[4] = q2.x, W[5] = q2.y;
+    } else {
+      // u8: three aligned words (voxels x-4 .. x+7), each byte pair widened
+      // into u16 lanes with one PRMT
+      const uint32_t* p = reinterpret_cast<const uint32_t*>(stage + roff + r * PB);
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const uint32_t b4 = p[i];
+        W[2 * i] = prmt(b4, 0u, 0x4140u);
+        W[2 * i + 1] = prmt(b4, 0u, 0x4342u);
+      }
+    }
     uint32_t P[5];  // P[i] = (hi of W[i], lo of W[i+1]): odd-start pairs
     // (IMAD.HI + IMAD on the idle FMA pipe instead of the PRMT measured 784
     // vs 831 Gvox/s: the IMAD.HI rate)
@@ -1378,7 +1404,7 @@ k_morph_u16s(const __grid_constant__ CUtensorMap tin, uint16_t* __restrict__ out
     unsigned char* stage = smem + st * G::PITCH;
     mbar_wait(&bar[st], ph);
     if (border) {
-      clamp_tile<uint16_t, MU_WARPS * 32>(reinterpret_cast<uint16_t*>(stage), MU_WBOX, G::HY, MU_WBOX,
+      clamp_tile<T, MU_WARPS * 32>(reinterpret_cast<T*>(stage), MU_WBOX, G::HY, MU_WBOX,
                                           y0 - R, x0 - MU_XA, a.ny, a.nx, tid);
       __syncthreads();
     }
@@ -1446,16 +1472,17 @@ k_morph_u16s(const __grid_constant__ CUtensorMap tin, uint16_t* __restrict__ out
     // output o = s - 2R is complete (slot (U + 1) mod RING)
     constexpr int cs = (U + 1) % RING;
     if (s >= 2 * R) {
-      uint16_t* op = obase + (int64_t)(s - 2 * R) * plane;
+      T* op = obase + (int64_t)(s - 2 * R) * plane;
 #pragma unroll
       for (int t = 0; t < MU_RO; ++t) {
         if (gy + t < a.ny) {
-          uint16_t* d = op + (int64_t)t * a.nx;
+          T* d = op + (int64_t)t * a.nx;
           if (st_full) {
-            *reinterpret_cast<uint2*>(d) = make_uint2(A[cs][t][0], A[cs][t][1]);
+            if constexpr (sizeof(T) == 2) *reinterpret_cast<uint2*>(d) = make_uint2(A[cs][t][0], A[cs][t][1]);
+            else *reinterpret_cast<uint32_t*>(d) = prmt(A[cs][t][0], A[cs][t][1], 0x6420);
           } else if (st_part) {
             for (int i = 0; i < 4 && gx + i < a.nx; ++i)
-              d[i] = (uint16_t)((A[cs][t][i >> 1] >> (16 * (i & 1))) & 0xffffu);
+              d[i] = (T)((A[cs][t][i >> 1] >> (16 * (i & 1))) & 0xffffu);
           }
         }
       }
@@ -1475,18 +1502,22 @@ k_morph_u16s(const __grid_constant__ CUtensorMap tin, uint16_t* __restrict__ out
 }
 
 // NotSupported outside the envelope (k_morph3 takes those): TMA layout (16-B
-// aligned base, nx % 8 == 0), extents < 2^30.  HB_MORPH_U16_SMEM=1 keeps
-// k_morph3 for u16 (A/B).
-template <bool MAX, int KIND, int R>
-cudaError_t launch_morph_u16s(const DevIn& in, int64_t zo, int64_t nzo, void* out, cudaStream_t s) {
-  using G = MUGeo<R>;
-  if (in.dt != HB_U16 || (in.nx % 8) != 0 || (reinterpret_cast<uintptr_t>(in.p) & 15) != 0 ||
-      in.nz >= (1 << 30) || in.ny >= (1 << 30) || in.nx >= (1 << 30) || std::getenv("HB_MORPH_U16_SMEM"))
+// aligned base, nx * sizeof(T) % 16 == 0), extents < 2^30.
+// HB_MORPH_U16_SMEM=1 / HB_MORPH_U8_SMEM=1 keep k_morph3 (A/B).
+template <typename T, bool MAX, int KIND, int R>
+cudaError_t launch_morph_u16s(const DevIn& in, int64_t zo, int64_t nzo, void* out, cudaStream_t s,
+                              const int* gate = nullptr) {
+  using G = MUGeo<T, R>;
+  constexpr int dt = sizeof(T) == 2 ? HB_U16 : HB_U8;
+  if (in.dt != dt || (in.nx % (16 / (int)sizeof(T))) != 0 || (reinterpret_cast<uintptr_t>(in.p) & 15) != 0 ||
+      in.nz >= (1 << 30) || in.ny >= (1 << 30) || in.nx >= (1 << 30) ||
+      std::getenv(sizeof(T) == 2 ? "HB_MORPH_U16_SMEM" : "HB_MORPH_U8_SMEM"))
     return cudaErrorNotSupported;
   CUtensorMap tin;
-  if (!make_tmap_3d(&tin, in.p, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, in.nx, in.ny, in.nz, MU_WBOX, G::HY))
+  if (!make_tmap_3d(&tin, in.p, sizeof(T) == 2 ? CU_TENSOR_MAP_DATA_TYPE_UINT16 : CU_TENSOR_MAP_DATA_TYPE_UINT8,
+                    (int)sizeof(T), in.nx, in.ny, in.nz, MUT<T>::WBOX, G::HY))
     return cudaErrorNotSupported;
-  auto kern = k_morph_u16s<MAX, KIND, R>;
+  auto kern = k_morph_u16s<T, MAX, KIND, R>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM) != cudaSuccess)
     return cudaErrorNotSupported;
   Morph3Args a;
@@ -1513,7 +1544,7 @@ cudaError_t launch_morph_u16s(const DevIn& in, int64_t zo, int64_t nzo, void* ou
   }
   a.zchunk = (int)std::min<int64_t>(zchunk, std::max<int64_t>(1, nzo));
   grid.z = (unsigned)((nzo + a.zchunk - 1) / a.zchunk);
-  kern<<<grid, MU_WARPS * 32, G::SMEM, s>>>(tin, (uint16_t*)out, a);
+  kern<<<grid, MU_WARPS * 32, G::SMEM, s>>>(tin, (T*)out, a, gate);
   return cudaGetLastError();
 }
 
@@ -1536,7 +1567,7 @@ template <typename T, bool MAX, int KIND, int R>
 cudaError_t launch_morph3(const DevIn& in, int64_t zo, int64_t nzo, void* out, cudaStream_t s,
                           int* gate_scratch) {
   if constexpr (sizeof(T) == 2) {
-    const cudaError_t e = launch_morph_u16s<MAX, KIND, R>(in, zo, nzo, out, s);
+    const cudaError_t e = launch_morph_u16s<uint16_t, MAX, KIND, R>(in, zo, nzo, out, s);
     if (e != cudaErrorNotSupported) return e;
     cudaGetLastError();
     return launch_morph3_v<T, MAX, KIND, R, false>(in, zo, nzo, out, nullptr, s);
@@ -1562,7 +1593,13 @@ cudaError_t launch_morph3(const DevIn& in, int64_t zo, int64_t nzo, void* out, c
       e = launch_morph_bits<MAX, KIND, R>(in, zo, nzo, out, gate, s);
     }
     if (e == cudaSuccess) {
-      e = launch_morph3_v<T, MAX, KIND, R, false>(in, zo, nzo, out, gate, s);
+      // grey blocks (flagged by the bits kernel): the u16-lane streaming
+      // kernel, else k_morph3
+      e = launch_morph_u16s<uint8_t, MAX, KIND, R>(in, zo, nzo, out, s, gate);
+      if (e == cudaErrorNotSupported) {
+        cudaGetLastError();
+        e = launch_morph3_v<T, MAX, KIND, R, false>(in, zo, nzo, out, gate, s);
+      }
       release();
       return e;
     }

@@ -64,6 +64,9 @@ def test_fuzz_morphology(oracle, case):
     assert np.array_equal(morphology.dilate(b, se), oracle.dilate(b, se.reflect().offsets)), (spec, b.shape)
     g = rng.integers(0, 65536, size=(nz, ny, nx + 4)).astype(np.uint16)  # k_morph3
     assert np.array_equal(morphology.erode(g, se), oracle.erode(g, se.offsets)), (spec, g.shape)
+    gb = rng.integers(0, 256, size=(nz, ny, nx)).astype(np.uint8)  # grey u8: bits2 flags it, k_morph_u16s<u8>
+    assert np.array_equal(morphology.erode(gb, se), oracle.erode(gb, se.offsets)), (spec, gb.shape)
+    assert np.array_equal(morphology.dilate(gb, se), oracle.dilate(gb, se.reflect().offsets)), (spec, gb.shape)
     nx8 = 8 * int(rng.integers(1, 70))  # k_morph_u16s: ragged 128-column tiles
     g = rng.integers(0, 65536, size=(nz, ny, nx8)).astype(np.uint16)
     assert np.array_equal(morphology.erode(g, se), oracle.erode(g, se.offsets)), (spec, g.shape)
