@@ -618,7 +618,7 @@ def side_filters(n, peak, stream):
                                      "kernel": "k_median5_net"}
     del x, o
     torch.cuda.synchronize()
-    # configs[2]: erosion ball:3 on 2048^2-plane slabs, u16 grey and u8 binary
+    # configs[2]: erosion ball:3 on 2048^2-plane slabs, u16 grey, u8 binary and u8 grey
     # (a 256-slice slab per launch: local ops are size-invariant per slice)
     from paper_2511_11890_b200 import morphology
 
@@ -629,14 +629,18 @@ def side_filters(n, peak, stream):
             ("erode_ball3_u16_2048", torch.uint16,
              lambda: torch.randint(0, 65536, (nzs + 6, m, m), device="cuda", dtype=torch.int32).to(torch.uint16), 4),
             ("erode_ball3_u8_binary_2048", torch.uint8,
-             lambda: (torch.rand((nzs + 6, m, m), device="cuda") < 0.5).to(torch.uint8), 2)):
+             lambda: (torch.rand((nzs + 6, m, m), device="cuda") < 0.5).to(torch.uint8), 2),
+            ("erode_ball3_u8_grey_2048", torch.uint8,
+             lambda: torch.randint(0, 256, (nzs + 6, m, m), device="cuda", dtype=torch.int32).to(torch.uint8), 2)):
         x = make()
         o = torch.empty((nzs, m, m), device="cuda", dtype=dt)
         ms = _timeit(lambda: _native.apply_device(x, o, prog, 3, stream), stream)
         v = m * m * nzs
         res[name] = {"gvox_s": round(v / ms / 1e6, 3), "ms": round(ms, 4),
                      "hbm_frac": round(bpv * v / ms / 1e6 / peak, 4),
-                     "kernel": "k_morph_u16s" if dt == torch.uint16 else "k_morph_bits2"}
+                     "kernel": {"erode_ball3_u16_2048": "k_morph_u16s",
+                                "erode_ball3_u8_binary_2048": "k_morph_bits2",
+                                "erode_ball3_u8_grey_2048": "k_morph_bits2 (grey flag) + k_morph_u16s<u8>"}[name]}
         del x, o
     torch.cuda.synchronize()
     return res
