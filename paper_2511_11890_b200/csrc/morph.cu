@@ -1099,14 +1099,24 @@ k_morph_bits2(const __grid_constant__ CUtensorMap tin, uint8_t* __restrict__ out
     tma_load_3d(d, &tin, x0 - 32, y0 - R, zin(k), &bar[stg]);
     tma_load_3d(d + G::BOXP, &tin, x0 - 32 + MB2_BOXW, y0 - R, zin(k), &bar[stg]);
   };
+  // a block already flagged grey by an earlier CTA: its output is void (the
+  // u16-lane kernel queued behind rewrites all of it), so later CTAs leave
+  // at once — decided by thread 0 before any TMA is issued, so the exit is
+  // CTA-uniform and leaves no copy in flight (grey u8 2048^2 x 256: the bits
+  // pass shrinks to ~its first wave)
+  __shared__ int s_skip;
   if (tid == 0) {
+    s_skip = *reinterpret_cast<volatile const int*>(grey_flag);
+    if (!s_skip) {
 #pragma unroll
-    for (int i = 0; i < MB2_NST; ++i) mbar_init(&bar[i], 1);
-    fence_mbar_init();
-    prefetch_tmap(&tin);
-    for (int i = 0; i < MB2_NST && i < nsl; ++i) load(i, i);
+      for (int i = 0; i < MB2_NST; ++i) mbar_init(&bar[i], 1);
+      fence_mbar_init();
+      prefetch_tmap(&tin);
+      for (int i = 0; i < MB2_NST && i < nsl; ++i) load(i, i);
+    }
   }
   __syncthreads();
+  if (s_skip) return;
   const bool border = x0 - 32 < 0 || x0 + MB2_TXW * 32 + 32 > nx || y0 - R < 0 || y0 + MB2_TYO + R > ny;
   // this thread: word w of the tile, output rows y0 + 2g, y0 + 2g + 1
   const int w = tid % MB2_TXW, g = tid / MB2_TXW;

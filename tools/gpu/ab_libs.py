@@ -3,7 +3,7 @@ of one operator on a synthetic volume, output checksum compared across builds.
 
 usage: python tools/gpu/ab_libs.py OP N lib1.so lib2.so ...
   OP: median (r=1 f32), gaussian (sigma=2 fast f32), erode_u16 (ball:3), median5 /
-  median5_u16 (r=2 on N x 1024^2)."""
+  median5_u16 (r=2 on N x 1024^2), erode_u8_grey / erode_u8_bin (ball:3, N x 2048^2)."""
 import json
 import os
 import subprocess
@@ -23,6 +23,13 @@ if op in ("median5", "median5_u16"):
         x = torch.randint(0, 65536, (n + 4, 1024, 1024), generator=g, device="cuda", dtype=torch.int32).to(torch.uint16)
     o = torch.empty((n, 1024, 1024), device="cuda", dtype=x.dtype)
     prog, zb = filters.median_program(2), 2
+elif op in ("erode_u8_grey", "erode_u8_bin"):
+    if op == "erode_u8_grey":
+        x = torch.randint(0, 256, (n + 6, 2048, 2048), generator=g, device="cuda", dtype=torch.int32).to(torch.uint8)
+    else:
+        x = (torch.rand((n + 6, 2048, 2048), generator=g, device="cuda") < 0.5).to(torch.uint8)
+    o = torch.empty((n, 2048, 2048), device="cuda", dtype=torch.uint8)
+    prog, zb = morphology.morph_program("erode", morphology.StructuringElement.ball(3)), 3
 elif op == "erode_u16":
     x = torch.randint(0, 65536, (n + 6, 2048, 2048), generator=g, device="cuda", dtype=torch.int32).to(torch.uint16)
     o = torch.empty((n, 2048, 2048), device="cuda", dtype=torch.uint16)
